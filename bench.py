@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Benchmark: clustered Mhit/s of the Timepix3 clustering hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the whole hot path (validate -> ToA sort -> window
+search + union-find -> labels -> compaction -> features) over one batch.
+N=1 workload: BASELINE.json configs[2] "mixed" (200M hits at a 40 Mhit/s
+shape, dots + MIP tracks, dt_max = 500 ns = 320 ticks) -- the config the
+metric is quoted on that fits one GPU.  Inputs (3.2 GB) exceed the 126 MB L2,
+so no flush is needed between steps.
+
+``--impl reference`` times the CPU oracle (oracle/, the plain single-threaded
+C BFS) on a bounded sample of the same workload: it is the reference arm of
+this tier (no upstream code exists).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "clustered Mhit/s at 1/2/4/8 B200 (device-timed); HBM GB/s as % of peak"
+PRESET = "mixed"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(h_sample, dt, label: str):
+    import oracle
+
+    t0 = time.perf_counter()
+    oracle.cluster(h_sample, dt)
+    t = time.perf_counter() - t0
+    return {"value": len(h_sample) / t / 1e6, "unit": "Mhit/s", "cores": 1, "kind": "oracle",
+            "sample": label, "seconds": round(t, 3),
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle, on the box's host cores (1 thread)."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import tpxgen
+
+    p = tpxgen.PRESETS[PRESET]
+    n_sample = args.ref_step_sample
+    h = tpxgen.generate(PRESET, n_hits=n_sample)
+    import oracle
+
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        oracle.cluster(h[: min(len(h), 200_000)], p["dt_max"])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.cluster(h, p["dt_max"])
+        times.append(time.perf_counter() - t0)
+    t = max(times) if times else float("nan")
+    val = n_sample / (sum(times) / len(times)) / 1e6
+    sample = f"first {n_sample} hits of {PRESET} (configs[2]) per step, single-threaded C oracle"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Mhit/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (tpxgen seeded generator)",
+        "config": {"workload": f"{PRESET}: configs[2] sample", "n_hits": n_sample,
+                   "dt_max_ticks": p["dt_max"], "sensor": "256x256"},
+        "cpu_baseline": {"value": val, "unit": "Mhit/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "Mhit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "max_step_s": t,
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        raise SystemExit("multi-GPU bench requires the sharded path (see DESIGN.md); run with --gpus 1")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2412_11809_b200 as tpx
+    import tpxgen
+
+    p = tpxgen.PRESETS[PRESET]
+    n = int(args.n_hits or p["n_hits"])
+    dt = p["dt_max"]
+    # ---- input: seeded synthetic stream, pinned host buffer, resident copy in HBM
+    t0 = time.time()
+    h_host = torch.empty(n * 16, dtype=torch.uint8).pin_memory()
+    tpxgen.generate(PRESET, n_hits=n, out=h_host.numpy())
+    gen_s = time.time() - t0
+    d_hits = h_host.to(dev, non_blocking=False)
+    c = tpx.Clusterer(dt)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    feats = torch.empty((n, 64), dtype=torch.uint8, device=dev)
+    wsbuf = torch.empty(c.workspace_bytes(n), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return c.run(d_hits, n=n, labels=labels, features=feats, capacity=n, workspace=wsbuf, stream=stream)
+
+    for _ in range(args.warmup):
+        _, _, k = step()
+    torch.cuda.synchronize()
+    c.set_profiling(True)
+    stage_tot: dict[str, float] = {}
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, _, k = step()
+            st = c.stats()
+            launches += st["kernel_launches"]
+            for name, ms in st["stage_ms"].items():
+                stage_tot[name] = stage_tot.get(name, 0.0) + ms
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    c.set_profiling(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    value = n / (ms * 1e-3) / 1e6  # Mhit/s
+    clocks = clk.summary()
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), H2D/D2H timed
+    cap_host = max(n // 4, 1)
+    lab_host = torch.empty(n, dtype=torch.int32).pin_memory()
+    feat_host = torch.empty((cap_host, 64), dtype=torch.uint8).pin_memory()
+    del wsbuf
+    torch.cuda.empty_cache()
+    hws = torch.empty(c.host_workspace_bytes(n, cap_host), dtype=torch.uint8, device=dev)
+    kk = c.run_host(h_host, lab_host, feat_host, capacity=cap_host, workspace=hws, stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        kk = c.run_host(h_host, lab_host, feat_host, capacity=cap_host, workspace=hws, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    del hws
+
+    # ---- roofline of the dominant kernel (B_alg = 16 + 4 + 64/s_bar per hit)
+    s_bar = n / max(k, 1)
+    b_alg_hit = 16 + 4 + 64 / s_bar
+    stage_avg = {k_: v / args.steps for k_, v in stage_tot.items()}
+    dom = max(stage_avg, key=stage_avg.get) if stage_avg else None
+    peak, peak_src = _peaks()
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if dom and os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(dom)
+        except Exception:
+            traffic = None
+    roof = None
+    if dom:
+        achieved = b_alg_hit * n / (stage_avg[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_hit": round(b_alg_hit, 3), "launch_ms": round(stage_avg[dom], 4)}
+    whole_path_gbs = b_alg_hit * n / (ms * 1e-3) / 1e9
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        ns = min(args.ref_sample, n)
+        sample = h_host[: ns * 16].numpy().view(tpxgen.HIT_DTYPE)
+        cpu = cpu_baseline(sample, dt, f"first {ns} hits of the same {PRESET} stream, single-threaded C oracle")
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mhit/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (tpxgen seeded generator, preset mixed)",
+        "config": {"workload": f"{PRESET} = BASELINE.json configs[2]: {n} hits, 40 Mhit/s shape, 80% gamma "
+                               f"dots + 20% MIP tracks, dt_max=500 ns", "n_hits": n, "dt_max_ticks": dt,
+                   "sensor": "256x256", "n_clusters": int(k),
+                   "l2": "inputs (16 B x n = %.1f GB) exceed L2 (126 MB); no flush" % (n * 16 / 1e9),
+                   "parallelism": f"{ws} GPU"},
+        "e2e": {"value": round(n / (e2e_ms * 1e-3) / 1e6, 2), "unit": "Mhit/s", "h2d_bytes_per_step": n * 16,
+                "d2h_bytes_per_step": n * 4 + min(kk, cap_host) * 64, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "hbm_alg_gbs_whole_path": round(whole_path_gbs, 2),
+        "hbm_frac_whole_path": round(whole_path_gbs / peak, 4),
+        "stage_ms": {k_: round(v, 4) for k_, v in stage_avg.items()},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gen_seconds": round(gen_s, 2),
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-hits", type=int, default=None, help="override the workload size (testing only)")
+    ap.add_argument("--ref-sample", type=int, default=16_000_000,
+                    help="hits per oracle step (bounded CPU sample, ~15 s)")
+    ap.add_argument("--ref-step-sample", type=int, default=4_000_000,
+                    help="hits per --impl reference step (~3.5 s of single-threaded CPU work)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

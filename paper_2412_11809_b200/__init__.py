@@ -1,0 +1,229 @@
+"""B200-native Timepix3 hit clustering (arXiv 2412.11809 hot path).
+
+Thin Python binding over the C-ABI library ``lib/libtpxcluster.so``
+(``include/tpx_cluster.h``): argument marshalling only.  Every step of the
+path -- ToA sort, windowed neighbour search, union-find, canonical labels,
+compaction, feature reductions, centroids -- runs in the library's sm_100a
+kernels.  PyTorch supplies device memory and streams.  There is no CPU
+fallback: if the library is missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libtpxcluster.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(or python paper_2412_11809_b200/build.py); there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+TPX_OK = 0
+TPX_ERR_CAPACITY = -5
+VARIANT_LOCAL, VARIANT_GLOBAL, VARIANT_STATIC = 0, 1, 2
+
+#: 64-byte cluster feature record (tpx_cluster_features).
+FEATURE_DTYPE = np.dtype(
+    [("label", "<u4"), ("size", "<u4"), ("toa_min", "<u8"), ("toa_max", "<u8"),
+     ("tot_sum", "<u8"), ("sum_x", "<u8"), ("sum_y", "<u8"), ("sum_tot_x", "<u8"),
+     ("sum_tot_y", "<u8")]
+)
+
+_vp, _u64, _u32, _int = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+
+
+class RunStats(ctypes.Structure):
+    _fields_ = [
+        ("n_hits", _u64), ("n_clusters", _u64), ("sort_path", _u32), ("sort_retries", _u32),
+        ("cross_pairs", _u64), ("kernel_launches", _u32), ("n_stages", _u32),
+        ("stage_ms", ctypes.c_float * 16),
+    ]
+
+
+def _proto(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_abi_version = _proto("tpx_abi_version", _int)
+_status_string = _proto("tpx_status_string", ctypes.c_char_p, _int)
+_create = _proto("tpx_cluster_create", _int, _u64, _int, _u32, _u32, ctypes.POINTER(_vp))
+_destroy = _proto("tpx_cluster_destroy", None, _vp)
+_ws_bytes = _proto("tpx_cluster_workspace_bytes", _int, _vp, _u64, ctypes.POINTER(ctypes.c_size_t))
+_run = _proto("tpx_cluster_run", _int, _vp, _vp, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp,
+              ctypes.c_size_t, _vp)
+_host_ws_bytes = _proto("tpx_cluster_host_workspace_bytes", _int, _vp, _u64, _u64,
+                        ctypes.POINTER(ctypes.c_size_t))
+_run_host = _proto("tpx_cluster_run_host", _int, _vp, _vp, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp,
+                   ctypes.c_size_t, _vp)
+_centroids = _proto("tpx_cluster_centroids", _int, _vp, _u64, _vp, _vp)
+_last_stats = _proto("tpx_cluster_last_stats", _int, _vp, ctypes.POINTER(RunStats))
+_set_profiling = _proto("tpx_cluster_set_profiling", _int, _vp, _int)
+_stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
+
+ABI_VERSION = _abi_version()
+
+
+class TpxError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+def status_string(status: int) -> str:
+    return _status_string(status).decode()
+
+
+def stage_name(i: int) -> str:
+    return _stage_name(i).decode()
+
+
+def _torch():
+    import torch  # plumbing only: device memory + streams
+
+    return torch
+
+
+def _stream_handle(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Clusterer:
+    """One library context (``tpx_cluster_create``); not thread-safe.
+
+    ``dt_max`` is in ToA ticks (1.5625 ns).  ``run`` takes a CUDA tensor of
+    n 16-byte ``tpx_hit`` records and returns ``(labels, features, n_clusters)``
+    as CUDA tensors (labels: int32 view of u32; features: uint8 [k, 64]).
+    """
+
+    def __init__(self, dt_max: int, width: int = 256, height: int = 256, variant: int = VARIANT_LOCAL):
+        h = _vp()
+        rc = _create(int(dt_max), int(variant), int(width), int(height), ctypes.byref(h))
+        if rc != TPX_OK:
+            raise TpxError(rc, "tpx_cluster_create")
+        self._h = h
+        self.dt_max, self.width, self.height = int(dt_max), int(width), int(height)
+        self._ws = None
+
+    # -- resources ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            _destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace_bytes(self, n: int) -> int:
+        b = ctypes.c_size_t(0)
+        rc = _ws_bytes(self._h, int(n), ctypes.byref(b))
+        if rc != TPX_OK:
+            raise TpxError(rc, "tpx_cluster_workspace_bytes")
+        return b.value
+
+    def host_workspace_bytes(self, n: int, capacity: int) -> int:
+        b = ctypes.c_size_t(0)
+        rc = _host_ws_bytes(self._h, int(n), int(capacity), ctypes.byref(b))
+        if rc != TPX_OK:
+            raise TpxError(rc, "tpx_cluster_host_workspace_bytes")
+        return b.value
+
+    def _workspace(self, nbytes: int, device):
+        torch = _torch()
+        if self._ws is None or self._ws.numel() < nbytes or self._ws.device != device:
+            self._ws = None
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self._ws
+
+    def set_profiling(self, on: bool = True):
+        _set_profiling(self._h, 1 if on else 0)
+
+    def stats(self) -> dict:
+        s = RunStats()
+        _last_stats(self._h, ctypes.byref(s))
+        d = {k: getattr(s, k) for k, _ in RunStats._fields_ if k != "stage_ms"}
+        d["stage_ms"] = {stage_name(i): s.stage_ms[i] for i in range(s.n_stages)}
+        return d
+
+    # -- the hot path ------------------------------------------------------
+    def run(self, hits, n: int | None = None, labels=None, features=None, capacity: int | None = None,
+            workspace=None, stream=None, check: bool = True):
+        """Cluster hits resident on the GPU (``tpx_cluster_run``)."""
+        torch = _torch()
+        assert hits.is_cuda and hits.is_contiguous()
+        if n is None:
+            n = hits.numel() * hits.element_size() // 16
+        dev = hits.device
+        if labels is None:
+            labels = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        if capacity is None:
+            capacity = n if features is None else features.numel() * features.element_size() // 64
+        if features is None:
+            features = torch.empty((max(capacity, 1), 64), dtype=torch.uint8, device=dev)
+        if workspace is None:
+            workspace = self._workspace(self.workspace_bytes(n), dev)
+        k = _u64(0)
+        rc = _run(self._h, hits.data_ptr(), int(n), labels.data_ptr(), features.data_ptr(), int(capacity),
+                  ctypes.byref(k), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                  _stream_handle(stream))
+        if check and rc not in (TPX_OK,):
+            raise TpxError(rc, "tpx_cluster_run")
+        kk = min(k.value, capacity)
+        return labels[:n], features[:kk], k.value
+
+    def run_host(self, hits_host, labels_host, features_host, capacity: int | None = None, workspace=None,
+                 stream=None, check: bool = True) -> int:
+        """End-to-end with HOST buffers (``tpx_cluster_run_host``).
+
+        ``hits_host`` / ``labels_host`` / ``features_host`` are CPU tensors
+        (pinned for asynchronous DMA) or numpy arrays; returns n_clusters.
+        """
+        def ptr(a):
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+        def nbytes(a):
+            return a.numel() * a.element_size() if hasattr(a, "numel") else a.nbytes
+
+        n = nbytes(hits_host) // 16
+        if capacity is None:
+            capacity = nbytes(features_host) // 64
+        torch = _torch()
+        if workspace is None:
+            workspace = self._workspace(self.host_workspace_bytes(n, capacity), torch.device("cuda"))
+        k = _u64(0)
+        rc = _run_host(self._h, ptr(hits_host), int(n), ptr(labels_host), ptr(features_host), int(capacity),
+                       ctypes.byref(k), workspace.data_ptr(), workspace.numel(), _stream_handle(stream))
+        if check and rc != TPX_OK:
+            raise TpxError(rc, "tpx_cluster_run_host")
+        return k.value
+
+
+def centroids(features, stream=None):
+    """fp64 ToT-weighted centroids [k, 2] of device feature records."""
+    torch = _torch()
+    k = features.numel() * features.element_size() // 64
+    out = torch.empty((max(k, 1), 2), dtype=torch.float64, device=features.device)
+    rc = _centroids(features.data_ptr(), int(k), out.data_ptr(), _stream_handle(stream))
+    if rc != TPX_OK:
+        raise TpxError(rc, "tpx_cluster_centroids")
+    return out[:k]
+
+
+def features_to_numpy(features) -> np.ndarray:
+    """Device/host feature bytes -> structured numpy array (FEATURE_DTYPE)."""
+    a = features.detach().cpu().contiguous().numpy() if hasattr(features, "detach") else np.asarray(features)
+    return a.reshape(-1).view(np.uint8).view(FEATURE_DTYPE)

@@ -1,0 +1,114 @@
+// common.cuh -- shared device types and helpers of the CUDA path (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tpx_cluster.h"
+
+namespace tpx {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Sorted hit record, 16 B, the in-HBM layout after the ToA sort (DESIGN.md
+// "HBM layout"): tt = toa << 16 | tot (toa < 2^48), xy = y << 16 | x,
+// idx = input index.  One 128-bit load gives everything the window search,
+// the union-find and the feature reductions need.
+struct __align__(16) srec {
+  uint64_t tt;
+  uint32_t xy;
+  uint32_t idx;
+};
+static_assert(sizeof(srec) == 16, "srec is 16 bytes");
+
+__device__ __forceinline__ uint64_t srec_toa(const srec& r) { return r.tt >> 16; }
+__device__ __forceinline__ uint32_t srec_tot(const srec& r) { return (uint32_t)(r.tt & 0xffffu); }
+__device__ __forceinline__ uint32_t srec_x(const srec& r) { return r.xy & 0xffffu; }
+__device__ __forceinline__ uint32_t srec_y(const srec& r) { return r.xy >> 16; }
+
+__device__ __forceinline__ srec load_srec(const srec* p) {
+  uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  srec r;
+  r.tt = (uint64_t)v.x | ((uint64_t)v.y << 32);
+  r.xy = v.z;
+  r.idx = v.w;
+  return r;
+}
+
+__device__ __forceinline__ void store_srec(srec* p, const srec& r) {
+  uint4 v;
+  v.x = (uint32_t)r.tt;
+  v.y = (uint32_t)(r.tt >> 32);
+  v.z = r.xy;
+  v.w = r.idx;
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+// Input hit (tpx_hit) as one 128-bit load.
+struct hit4 {
+  uint64_t toa;
+  uint32_t x, y, tot;
+};
+__device__ __forceinline__ hit4 load_hit(const tpx_hit* h) {
+  uint4 v = __ldg(reinterpret_cast<const uint4*>(h));
+  hit4 r;
+  r.toa = (uint64_t)v.x | ((uint64_t)v.y << 32);
+  r.x = v.z & 0xffffu;
+  r.y = v.z >> 16;
+  r.tot = v.w & 0xffffu;
+  return r;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Coherent (L2) load: parent pointers are written concurrently by other CTAs.
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------- union-find
+// Parent forest over sorted positions (§4.1 l.215).  Links always go
+// from the larger root index to the smaller one, so parent(v) <= v, roots are
+// the earliest hit of their tree in (ToA, input index) order and the paper's
+// time-invariant toa(h) >= toa(parent(h)) (l.219-221) holds by construction.
+// find() compresses paths by halving (l.221, "path compression").
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
+  uint32_t cur = ld_cg(parent + v);
+  if (cur != v) {
+    uint32_t prev = v, next;
+    while (cur > (next = ld_cg(parent + cur))) {
+      parent[prev] = next;   // benign race: next is an ancestor of prev
+      prev = cur;
+      cur = next;
+    }
+  }
+  return cur;
+}
+
+// Read-only find for the flatten pass: path-halving stores from other threads
+// could otherwise overwrite a root another thread has just stored.
+__device__ __forceinline__ uint32_t uf_root(const uint32_t* parent, uint32_t v) {
+  uint32_t cur = ld_cg(parent + v), next;
+  while (cur != (next = ld_cg(parent + cur))) cur = next;
+  return cur;
+}
+
+// Lock-free union by atomicCAS on the larger root (ECL-CC style hooking).
+__device__ __forceinline__ void uf_unite(uint32_t* parent, uint32_t a, uint32_t b) {
+  uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+  while (ra != rb) {
+    if (ra < rb) {
+      uint32_t old = atomicCAS(parent + rb, rb, ra);
+      if (old == rb) break;
+      rb = old;
+    } else {
+      uint32_t old = atomicCAS(parent + ra, ra, rb);
+      if (old == ra) break;
+      ra = old;
+    }
+  }
+}
+
+}  // namespace tpx

@@ -1,0 +1,153 @@
+// sort.cuh -- ToA sort (Alg. GPU Step 3: "Sort hits by their
+// time of arrival. A fast option is the parallel radix sort").
+//
+// Global LSD radix sort on key = toa - toa_min with the input index as the
+// payload; every pass is stable, so the final order is (toa, input index).
+#pragma once
+#include "common.cuh"
+
+namespace tpx {
+
+struct dev_hdr {
+  unsigned long long toa_min;
+  unsigned long long toa_max;
+  unsigned int err;          // bit 0: coordinate / ToA range violation
+  unsigned int sort_bad;     // windowed-sort verification failures
+  unsigned long long n_clusters;
+  unsigned long long n_pairs;
+  unsigned long long pad[3];
+};
+
+constexpr int kMMThreads = 256;
+
+// Fused validation + min/max ToA (one read of the hits).
+__global__ void __launch_bounds__(kMMThreads) k_validate_minmax(const tpx_hit* __restrict__ hits, uint64_t n,
+                                                                uint32_t width, uint32_t height,
+                                                                dev_hdr* hdr) {
+  uint64_t mn = ~0ull, mx = 0;
+  unsigned bad = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    hit4 h = load_hit(hits + i);
+    mn = min(mn, h.toa);
+    mx = max(mx, h.toa);
+    bad |= (h.x >= width) | (h.y >= height) | (h.toa >> 48 != 0);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    bad |= __shfl_xor_sync(kFull, bad, o);
+  }
+  if (lane_id() == 0) {
+    atomicMin(&hdr->toa_min, mn);
+    atomicMax(&hdr->toa_max, mx);
+    if (bad) atomicOr(&hdr->err, 1u);
+  }
+}
+
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 keys per tile
+constexpr int kRadixBins = 256;
+
+template <typename KeyT, bool kFromHits>
+__device__ __forceinline__ KeyT radix_key(const tpx_hit* hits, const KeyT* keys, uint64_t i, uint64_t toa_min) {
+  if constexpr (kFromHits) {
+    return (KeyT)(load_hit(hits + i).toa - toa_min);
+  } else {
+    return keys[i];
+  }
+}
+
+// Per-tile digit histogram, written digit-major: hist[d * n_tiles + tile].
+template <typename KeyT, bool kFromHits>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const tpx_hit* __restrict__ hits,
+                                                             const KeyT* __restrict__ keys, uint64_t n,
+                                                             uint64_t toa_min, int shift,
+                                                             uint32_t* __restrict__ hist, uint32_t n_tiles) {
+  __shared__ uint32_t h[kRadixBins];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kRadixTile;
+#pragma unroll 4
+  for (int r = 0; r < kRadixItems; ++r) {
+    uint64_t i = base + (uint64_t)r * kRadixThreads + threadIdx.x;
+    unsigned d = 256;
+    if (i < n) d = (unsigned)((radix_key<KeyT, kFromHits>(hits, keys, i, toa_min) >> shift) & 0xffu);
+    unsigned peers = __match_any_sync(kFull, d);
+    if (d < 256 && (__ffs(peers) - 1) == (int)lane_id()) atomicAdd(&h[d], (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  hist[(uint64_t)threadIdx.x * n_tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: rank = global digit offset of this tile + number of earlier
+// (round, warp, lane)-ordered elements of the tile with the same digit.
+template <typename KeyT, bool kFromHits>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const tpx_hit* __restrict__ hits,
+                                                                const KeyT* __restrict__ keys_in,
+                                                                const uint32_t* __restrict__ vals_in, uint64_t n,
+                                                                uint64_t toa_min, int shift,
+                                                                const uint32_t* __restrict__ offsets,
+                                                                uint32_t n_tiles, KeyT* __restrict__ keys_out,
+                                                                uint32_t* __restrict__ vals_out) {
+  constexpr int kWarps = kRadixThreads / 32;
+  __shared__ uint32_t base[kRadixBins];
+  __shared__ uint32_t wcnt[kWarps][kRadixBins];
+  base[threadIdx.x] = offsets[(uint64_t)threadIdx.x * n_tiles + blockIdx.x];
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) wcnt[w][threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  const uint64_t tbase = (uint64_t)blockIdx.x * kRadixTile;
+  for (int r = 0; r < kRadixItems; ++r) {
+    uint64_t i = tbase + (uint64_t)r * kRadixThreads + threadIdx.x;
+    bool valid = i < n;
+    KeyT key = 0;
+    uint32_t val = 0;
+    unsigned d = 256;
+    if (valid) {
+      key = radix_key<KeyT, kFromHits>(hits, keys_in, i, toa_min);
+      val = kFromHits ? (uint32_t)i : vals_in[i];
+      d = (unsigned)((key >> shift) & 0xffu);
+    }
+    unsigned peers = __match_any_sync(kFull, d);
+    unsigned lrank = __popc(peers & lanemask_lt());
+    if (valid && lrank == 0) wcnt[warp][d] = (uint32_t)__popc(peers);
+    __syncthreads();
+    if (valid) {
+      uint32_t pos = base[d] + lrank;
+      for (unsigned w = 0; w < warp; ++w) pos += wcnt[w][d];
+      keys_out[pos] = key;
+      vals_out[pos] = val;
+    }
+    __syncthreads();
+    uint32_t add = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      add += wcnt[w][threadIdx.x];
+      wcnt[w][threadIdx.x] = 0;
+    }
+    base[threadIdx.x] += add;
+    __syncthreads();
+  }
+}
+
+// Sorted records + union-find init: rec[i] = hit[perm[i]], parent[i] = i.
+__global__ void k_gather_init(const tpx_hit* __restrict__ hits, const uint32_t* __restrict__ perm, uint64_t n,
+                              srec* __restrict__ rec, uint32_t* __restrict__ parent) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t j = perm ? perm[i] : (uint32_t)i;
+    hit4 h = load_hit(hits + j);
+    srec r;
+    r.tt = (h.toa << 16) | h.tot;
+    r.xy = (h.y << 16) | h.x;
+    r.idx = j;
+    store_srec(rec + i, r);
+    parent[i] = (uint32_t)i;
+  }
+}
+
+}  // namespace tpx

@@ -1,0 +1,375 @@
+// tpx_cluster.cu -- the C ABI (include/tpx_cluster.h) over the sm_100a kernels.
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "cluster.cuh"
+#include "common.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+using namespace tpx;
+
+namespace {
+
+constexpr int kMaxStages = 16;
+const char* const kStageNames[kMaxStages] = {
+    "validate", "sort", "gather", "union", "flatten", "labels", "compact", "features",
+    "", "", "", "", "", "", "", ""};
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct layout {
+  size_t hdr, keys0, keys1, vals0, vals1, rec, parent, minidx, flags, ord, hist, partials, total;
+};
+
+uint32_t n_tiles_of(uint64_t n, int tile) { return (uint32_t)((n + tile - 1) / tile); }
+
+layout make_layout(uint64_t n) {
+  layout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const uint32_t rt = n_tiles_of(n, kRadixTile);
+  const uint32_t st_hist = n_tiles_of((uint64_t)rt * kRadixBins, kScanTile);
+  const uint32_t st_n = n_tiles_of(n, kScanTile);
+  L.hdr = take(sizeof(dev_hdr));
+  L.keys0 = take(n * 8);
+  L.keys1 = take(n * 8);
+  L.vals0 = take(n * 4);
+  L.vals1 = take(n * 4);
+  L.rec = take(n * 16);
+  L.parent = take(n * 4);
+  L.minidx = take(n * 4);
+  L.flags = take(n * 4);
+  L.ord = take(n * 4);
+  L.hist = take((size_t)rt * kRadixBins * 4);
+  L.partials = take((size_t)(st_hist > st_n ? st_hist : st_n) * 4 + 4);
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+struct tpx_cluster {
+  uint64_t dt;
+  int variant;
+  uint32_t width, height;
+  dev_hdr* host_hdr;  // pinned
+  int profiling;
+  cudaEvent_t ev[kMaxStages + 1];
+  tpx_run_stats stats;
+  int cuda_ready;  // CUDA resources are created lazily by the first run
+};
+
+// Pinned header + timing events, created on first use so that contexts can be
+// created (and arguments validated) on a machine without a GPU.
+static int ensure_cuda(tpx_cluster* c) {
+  if (c->cuda_ready) return TPX_OK;
+  if (cudaMallocHost(&c->host_hdr, sizeof(dev_hdr)) != cudaSuccess) return TPX_ERR_CUDA;
+  for (int i = 0; i <= kMaxStages; ++i) {
+    if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
+      for (int k = 0; k < i; ++k) cudaEventDestroy(c->ev[k]);
+      cudaFreeHost(c->host_hdr);
+      return TPX_ERR_CUDA;
+    }
+  }
+  c->cuda_ready = 1;
+  return TPX_OK;
+}
+
+#define TPX_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      fprintf(stderr, "tpx_cluster: %s failed: %s\n", #call, cudaGetErrorString(e_));   \
+      return TPX_ERR_CUDA;                                                               \
+    }                                                                                    \
+  } while (0)
+
+#define TPX_LAUNCHED(ctx)                                                                \
+  do {                                                                                   \
+    (ctx)->stats.kernel_launches++;                                                      \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) {                                                             \
+      fprintf(stderr, "tpx_cluster: launch failed: %s\n", cudaGetErrorString(e_));       \
+      return TPX_ERR_CUDA;                                                               \
+    }                                                                                    \
+  } while (0)
+
+static int grid_for(uint64_t n, int threads) {
+  uint64_t g = (n + threads - 1) / threads;
+  const uint64_t cap = 148ull * 32;  // grid-stride loops beyond 32 CTAs per SM
+  if (g > cap) g = cap;
+  return (int)(g ? g : 1);
+}
+
+static int exclusive_scan(tpx_cluster* c, const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* partials,
+                          uint32_t* total, cudaStream_t s) {
+  uint32_t tiles = n_tiles_of(n, kScanTile);
+  k_scan_reduce<<<tiles, kScanThreads, 0, s>>>(in, n, partials);
+  TPX_LAUNCHED(c);
+  k_scan_partials<<<1, kScanThreads, 0, s>>>(partials, tiles, total);
+  TPX_LAUNCHED(c);
+  k_scan_down<<<tiles, kScanThreads, 0, s>>>(in, n, partials, out);
+  TPX_LAUNCHED(c);
+  return TPX_OK;
+}
+
+template <typename KeyT>
+static int radix_sort(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t toa_min, int passes, char* ws,
+                      const layout& L, uint32_t** perm_out, cudaStream_t s) {
+  KeyT* k0 = (KeyT*)(ws + L.keys0);
+  KeyT* k1 = (KeyT*)(ws + L.keys1);
+  uint32_t* v0 = (uint32_t*)(ws + L.vals0);
+  uint32_t* v1 = (uint32_t*)(ws + L.vals1);
+  uint32_t* hist = (uint32_t*)(ws + L.hist);
+  uint32_t* partials = (uint32_t*)(ws + L.partials);
+  const uint32_t tiles = n_tiles_of(n, kRadixTile);
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    if (p == 0) {
+      k_radix_hist<KeyT, true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, n, toa_min, shift, hist, tiles);
+    } else {
+      k_radix_hist<KeyT, false><<<tiles, kRadixThreads, 0, s>>>(hits, k0, n, toa_min, shift, hist, tiles);
+    }
+    TPX_LAUNCHED(c);
+    int rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s);
+    if (rc) return rc;
+    if (p == 0) {
+      k_radix_scatter<KeyT, true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, shift, hist,
+                                                                  tiles, k1, v1);
+    } else {
+      k_radix_scatter<KeyT, false><<<tiles, kRadixThreads, 0, s>>>(hits, k0, v0, n, toa_min, shift, hist, tiles,
+                                                                   k1, v1);
+    }
+    TPX_LAUNCHED(c);
+    KeyT* tk = k0; k0 = k1; k1 = tk;
+    uint32_t* tv = v0; v0 = v1; v1 = tv;
+  }
+  *perm_out = passes ? v0 : nullptr;
+  return TPX_OK;
+}
+
+extern "C" {
+
+int tpx_abi_version(void) { return TPX_ABI_VERSION; }
+
+const char* tpx_status_string(int s) {
+  switch (s) {
+    case TPX_OK: return "ok";
+    case TPX_ERR_INVALID_ARG: return "invalid argument";
+    case TPX_ERR_UNSUPPORTED: return "unsupported (only variant (iii)(a) LOCAL runs on the GPU)";
+    case TPX_ERR_COORD_RANGE: return "hit coordinate outside the sensor or toa >= 2^48";
+    case TPX_ERR_TOO_MANY_HITS: return "too many hits (n must be < 2^32 - 1)";
+    case TPX_ERR_CAPACITY: return "feature capacity too small (n_clusters_out holds the required count)";
+    case TPX_ERR_OOM: return "workspace too small";
+    case TPX_ERR_CUDA: return "CUDA error";
+    case TPX_ERR_NCCL: return "NCCL error";
+    default: return "unknown status";
+  }
+}
+
+const char* tpx_cluster_stage_name(int i) { return (i >= 0 && i < kMaxStages) ? kStageNames[i] : ""; }
+
+int tpx_cluster_create(uint64_t dt_max_ticks, int variant, uint32_t width, uint32_t height, tpx_cluster** out) {
+  if (!out) return TPX_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (variant < TPX_VARIANT_LOCAL || variant > TPX_VARIANT_STATIC) return TPX_ERR_INVALID_ARG;
+  if (width == 0 || height == 0 || width > 65535 || height > 65535) return TPX_ERR_INVALID_ARG;
+  if (dt_max_ticks >= (1ull << 48)) return TPX_ERR_INVALID_ARG;
+  if (variant != TPX_VARIANT_LOCAL) return TPX_ERR_UNSUPPORTED;
+  tpx_cluster* c = new (std::nothrow) tpx_cluster;
+  if (!c) return TPX_ERR_OOM;
+  memset(c, 0, sizeof(*c));
+  c->dt = dt_max_ticks;
+  c->variant = variant;
+  c->width = width;
+  c->height = height;
+  *out = c;
+  return TPX_OK;
+}
+
+void tpx_cluster_destroy(tpx_cluster* c) {
+  if (!c) return;
+  if (c->cuda_ready) {
+    for (int i = 0; i <= kMaxStages; ++i) cudaEventDestroy(c->ev[i]);
+    cudaFreeHost(c->host_hdr);
+  }
+  delete c;
+}
+
+int tpx_cluster_workspace_bytes(const tpx_cluster* c, uint64_t n, size_t* bytes) {
+  if (!c || !bytes) return TPX_ERR_INVALID_ARG;
+  if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
+  *bytes = make_layout(n).total;
+  return TPX_OK;
+}
+
+int tpx_cluster_set_profiling(tpx_cluster* c, int enable) {
+  if (!c) return TPX_ERR_INVALID_ARG;
+  c->profiling = enable ? 1 : 0;
+  return TPX_OK;
+}
+
+int tpx_cluster_last_stats(const tpx_cluster* c, tpx_run_stats* out) {
+  if (!c || !out) return TPX_ERR_INVALID_ARG;
+  *out = c->stats;
+  return TPX_OK;
+}
+
+int tpx_cluster_run(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* labels_out,
+                    tpx_cluster_features* features_out, uint64_t capacity, uint64_t* n_clusters_out, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (!c || !n_clusters_out) return TPX_ERR_INVALID_ARG;
+  *n_clusters_out = 0;
+  if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
+  memset(&c->stats, 0, sizeof(c->stats));
+  c->stats.n_hits = n;
+  if (n == 0) return TPX_OK;
+  if (!hits || !labels_out || !workspace || (!features_out && capacity)) return TPX_ERR_INVALID_ARG;
+  if (((uintptr_t)hits & 15) || ((uintptr_t)workspace & 255) || ((uintptr_t)features_out & 15) ||
+      ((uintptr_t)labels_out & 3))
+    return TPX_ERR_INVALID_ARG;
+  const layout L = make_layout(n);
+  if (workspace_bytes < L.total) return TPX_ERR_OOM;
+  if (ensure_cuda(c)) return TPX_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
+  srec* rec = (srec*)(ws + L.rec);
+  uint32_t* parent = (uint32_t*)(ws + L.parent);
+  uint32_t* minidx = (uint32_t*)(ws + L.minidx);
+  uint32_t* flags = (uint32_t*)(ws + L.flags);
+  uint32_t* ord = (uint32_t*)(ws + L.ord);
+  uint32_t* partials = (uint32_t*)(ws + L.partials);
+  int st = 0;
+  auto mark = [&](int stage) {
+    if (c->profiling) {
+      cudaEventRecord(c->ev[stage], s);
+      st = stage;
+    }
+  };
+
+  // ---- A2 validate + min/max ToA
+  mark(0);
+  dev_hdr init;
+  memset(&init, 0, sizeof(init));
+  init.toa_min = ~0ull;
+  TPX_CUDA(cudaMemcpyAsync(hdr, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  k_validate_minmax<<<grid_for(n, kMMThreads) < 148 * 8 ? grid_for(n, kMMThreads) : 148 * 8, kMMThreads, 0, s>>>(
+      hits, n, c->width, c->height, hdr);
+  TPX_LAUNCHED(c);
+  TPX_CUDA(cudaMemcpyAsync(c->host_hdr, hdr, sizeof(dev_hdr), cudaMemcpyDeviceToHost, s));
+  TPX_CUDA(cudaStreamSynchronize(s));
+  if (c->host_hdr->err) return TPX_ERR_COORD_RANGE;
+  const uint64_t toa_min = c->host_hdr->toa_min, range = c->host_hdr->toa_max - toa_min;
+  const int bits = range ? 64 - __builtin_clzll(range) : 0;
+  const int passes = (bits + 7) / 8;
+
+  // ---- A2 ToA sort (stable LSD radix on toa - min, payload = input index)
+  mark(1);
+  uint32_t* perm = nullptr;
+  int rc = (bits <= 32) ? radix_sort<uint32_t>(c, hits, n, toa_min, passes, ws, L, &perm, s)
+                        : radix_sort<uint64_t>(c, hits, n, toa_min, passes, ws, L, &perm, s);
+  if (rc) return rc;
+  c->stats.sort_path = 1;
+  mark(2);
+  k_gather_init<<<grid_for(n, 256), 256, 0, s>>>(hits, perm, n, rec, parent);
+  TPX_LAUNCHED(c);
+
+  // ---- A3 + A4 window search + union-find
+  mark(3);
+  k_window_union<<<grid_for(n, 256), 256, 0, s>>>(rec, n, c->dt, parent);
+  TPX_LAUNCHED(c);
+  mark(4);
+  k_flatten<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
+  TPX_LAUNCHED(c);
+
+  // ---- A5 canonical labels
+  mark(5);
+  TPX_CUDA(cudaMemsetAsync(minidx, 0xff, n * 4, s));
+  k_minidx<<<grid_for(n, 256), 256, 0, s>>>(rec, parent, n, minidx);
+  TPX_LAUNCHED(c);
+  k_labels<<<grid_for(n, 256), 256, 0, s>>>(rec, parent, minidx, n, labels_out);
+  TPX_LAUNCHED(c);
+
+  // ---- A6 compaction: ordinal of every label
+  mark(6);
+  k_flags<<<grid_for(n, 256), 256, 0, s>>>(labels_out, n, flags);
+  TPX_LAUNCHED(c);
+  rc = exclusive_scan(c, flags, n, ord, partials, (uint32_t*)&hdr->n_clusters, s);
+  if (rc) return rc;
+
+  // ---- A7 features
+  mark(7);
+  if (capacity) {
+    k_feat_init<<<grid_for(n, 256), 256, 0, s>>>(labels_out, ord, n, features_out, capacity);
+    TPX_LAUNCHED(c);
+    k_feat_accum<<<grid_for(n, 256), 256, 0, s>>>(rec, parent, minidx, ord, n, features_out, capacity);
+    TPX_LAUNCHED(c);
+  }
+  if (c->profiling) cudaEventRecord(c->ev[8], s);
+  TPX_CUDA(cudaMemcpyAsync(c->host_hdr, hdr, sizeof(dev_hdr), cudaMemcpyDeviceToHost, s));
+  TPX_CUDA(cudaStreamSynchronize(s));
+  const uint64_t k = (uint32_t)c->host_hdr->n_clusters;  // low word written by the scan
+  *n_clusters_out = k;
+  c->stats.n_clusters = k;
+  if (c->profiling) {
+    c->stats.n_stages = 8;
+    for (int i = 0; i < 8; ++i) cudaEventElapsedTime(&c->stats.stage_ms[i], c->ev[i], c->ev[i + 1]);
+  }
+  (void)st;
+  return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
+}
+
+int tpx_cluster_host_workspace_bytes(const tpx_cluster* c, uint64_t n, uint64_t capacity, size_t* bytes) {
+  if (!c || !bytes) return TPX_ERR_INVALID_ARG;
+  if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
+  *bytes = align256(n * 16) + align256(n * 4) + align256(capacity * 64) + make_layout(n).total;
+  return TPX_OK;
+}
+
+int tpx_cluster_run_host(tpx_cluster* c, const tpx_hit* hits_host, uint64_t n, uint32_t* labels_host,
+                         tpx_cluster_features* features_host, uint64_t capacity, uint64_t* n_clusters_out,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (!c || !n_clusters_out) return TPX_ERR_INVALID_ARG;
+  *n_clusters_out = 0;
+  if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
+  if (n == 0) return TPX_OK;
+  if (!hits_host || !labels_host || !workspace || (!features_host && capacity)) return TPX_ERR_INVALID_ARG;
+  size_t need = 0;
+  tpx_cluster_host_workspace_bytes(c, n, capacity, &need);
+  if (workspace_bytes < need) return TPX_ERR_OOM;
+  if ((uintptr_t)workspace & 255) return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  tpx_hit* d_hits = (tpx_hit*)ws;
+  uint32_t* d_labels = (uint32_t*)(ws + align256(n * 16));
+  tpx_cluster_features* d_feats = (tpx_cluster_features*)(ws + align256(n * 16) + align256(n * 4));
+  char* inner = ws + align256(n * 16) + align256(n * 4) + align256(capacity * 64);
+  size_t inner_bytes = workspace_bytes - (size_t)(inner - ws);
+  TPX_CUDA(cudaMemcpyAsync(d_hits, hits_host, n * 16, cudaMemcpyHostToDevice, s));
+  uint64_t k = 0;
+  int rc = tpx_cluster_run(c, d_hits, n, d_labels, d_feats, capacity, &k, inner, inner_bytes, stream);
+  if (rc != TPX_OK && rc != TPX_ERR_CAPACITY) return rc;
+  *n_clusters_out = k;
+  TPX_CUDA(cudaMemcpyAsync(labels_host, d_labels, n * 4, cudaMemcpyDeviceToHost, s));
+  uint64_t kk = k < capacity ? k : capacity;
+  if (kk) TPX_CUDA(cudaMemcpyAsync(features_host, d_feats, kk * 64, cudaMemcpyDeviceToHost, s));
+  TPX_CUDA(cudaStreamSynchronize(s));
+  return rc;
+}
+
+int tpx_cluster_centroids(const tpx_cluster_features* features, uint64_t k, double* cxy, void* stream) {
+  if (k == 0) return TPX_OK;
+  if (!features || !cxy) return TPX_ERR_INVALID_ARG;
+  k_centroids<<<grid_for(k, 256), 256, 0, (cudaStream_t)stream>>>(features, k, cxy);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TPX_OK : TPX_ERR_CUDA;
+}
+
+}  // extern "C"

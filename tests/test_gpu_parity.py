@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bit-exact labels and integer features on the same seeded inputs; centroids
+within relative 1e-12 (north_star; expected bit-identical, reading R9).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import tpxgen
+from tests import golden_examples, pins
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tpx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_11809_b200 import build
+
+    build.build()
+    import paper_2412_11809_b200 as p
+
+    return p
+
+
+_ctx_cache = {}
+
+
+def _gpu(tpx, h, dt, W=256, H=256, capacity=None):
+    key = (dt, W, H)
+    if key not in _ctx_cache:
+        _ctx_cache[key] = tpx.Clusterer(dt, W, H)
+    c = _ctx_cache[key]
+    n = len(h)
+    d = torch.from_numpy(np.ascontiguousarray(h).view(np.uint8).reshape(-1)).cuda() if n else \
+        torch.empty(16, dtype=torch.uint8, device="cuda")
+    labels, feats, k = c.run(d, n=n, capacity=capacity)
+    cxy = tpx.centroids(feats)
+    torch.cuda.synchronize()
+    return (labels.cpu().numpy().view(np.uint32)[:n], tpx.features_to_numpy(feats), k,
+            cxy.cpu().numpy(), c.stats())
+
+
+def _assert_parity(tpx, h, dt, W=256, H=256, ctx=""):
+    gl, gf, k, gc, st = _gpu(tpx, h, dt, W, H)
+    rl, rf = oracle.cluster(h, dt, W, H)
+    assert k == len(rf), f"{ctx}: n_clusters {k} vs {len(rf)}"
+    bad = np.nonzero(gl != rl)[0]
+    assert len(bad) == 0, f"{ctx}: {len(bad)} labels differ, first {bad[:5]}: {gl[bad[:5]]} vs {rl[bad[:5]]}"
+    if gf.tobytes() != rf.tobytes():
+        for name in pins.FEAT_FIELDS:
+            d = np.nonzero(gf[name] != rf[name])[0]
+            assert len(d) == 0, f"{ctx}: feature {name} differs at {d[:5]}"
+    rc = oracle.centroids(rf)
+    if len(rc):
+        rel = np.abs(gc - rc) / np.maximum(np.abs(rc), 1e-300)
+        assert rel.max() <= 1e-12, f"{ctx}: centroid rel err {rel.max()}"
+        assert np.array_equal(gc, rc), f"{ctx}: centroids not bit-identical"
+    return st
+
+
+# ----------------------------------------------------------------- examples
+EXAMPLES = golden_examples.load()
+
+
+@pytest.mark.parametrize("ex", EXAMPLES, ids=[e.eid for e in EXAMPLES])
+def test_golden_examples_gpu(tpx, ex):
+    gl, gf, k, _, _ = _gpu(tpx, ex.hits, ex.dt, ex.width, ex.height)
+    if ex.labels is not None:
+        assert gl.tolist() == ex.labels
+    if ex.nclusters is not None:
+        assert k == ex.nclusters
+    for want in ex.features:
+        row = gf[gf["label"] == want["label"]]
+        assert len(row) == 1
+        for key, v in want.items():
+            assert int(row[0][key]) == v
+
+
+# --------------------------------------------------------------- fuzz parity
+def test_fuzz_small_sensors(tpx):
+    rng = np.random.default_rng(2024)
+    for trial in range(150):
+        W, H = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        dt = int(rng.choice([0, 1, 3, 16, 128]))
+        n = int(rng.integers(1, 3000))
+        h = tpxgen.random_small(rng, n, W, H, max(4 * dt, 3))
+        _assert_parity(tpx, h, dt, W, H, ctx=f"trial {trial}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 4095, 4096, 4097, 8191, 65537, 300_001])
+def test_sizes_spanning_tiles(tpx, n):
+    h = tpxgen.generate("mixed", n_hits=n)
+    _assert_parity(tpx, h, 320, ctx=f"n={n}")
+
+
+@pytest.mark.parametrize("preset,n", [("tiny", None), ("lowflux", 2_000_000), ("mixed", 3_000_000),
+                                      ("heavyion", 1_000_000), ("timepix4", 2_000_000)])
+def test_presets(tpx, preset, n):
+    p = tpxgen.PRESETS[preset]
+    h = tpxgen.generate(preset, n_hits=n)
+    W, H = (448, 512) if preset == "timepix4" else (256, 256)
+    _assert_parity(tpx, h, p["dt_max"], W, H, ctx=preset)
+
+
+def test_lowflux_full_config(tpx):
+    # BASELINE.json configs[1] at its full size (10M hits)
+    h = tpxgen.generate("lowflux")
+    _assert_parity(tpx, h, 128, ctx="lowflux-10M")
+
+
+@pytest.mark.parametrize("dt", [0, 1, 64, 1000, 100_000])
+def test_dt_sweep(tpx, dt):
+    h = tpxgen.generate("mixed", n_hits=200_000)
+    _assert_parity(tpx, h, dt, ctx=f"dt={dt}")
+
+
+# -------------------------------------------------------------- edge cases
+def test_empty_and_degenerate(tpx):
+    gl, gf, k, _, _ = _gpu(tpx, np.zeros(0, dtype=tpxgen.HIT_DTYPE), 128)
+    assert k == 0
+    # all hits on one pixel at one time: one cluster
+    h = tpxgen.make_hits([(7, 7, 1000, 3)] * 5000)
+    _assert_parity(tpx, h, 0, ctx="one pixel")
+    # a diagonal chain over the whole sensor, each step exactly dt apart
+    h = tpxgen.make_hits([(i % 256, i % 256, i * 128, 1) for i in range(20000)])
+    _assert_parity(tpx, h, 128, ctx="chain")
+    # reverse-sorted input
+    h = tpxgen.generate("mixed", n_hits=100_000)[::-1].copy()
+    _assert_parity(tpx, h, 320, ctx="reversed")
+    # ToA near 2^48 and large ToA span (> 32 bits of key)
+    h = tpxgen.generate("mixed", n_hits=50_000)
+    h["toa"][::7] += np.uint64(1 << 40)
+    h["toa"] += np.uint64((1 << 47))
+    _assert_parity(tpx, h, 320, ctx="wide toa")
+
+
+def test_disorder_stress(tpx):
+    # paper-bound readout disorder t = 600 us
+    h = tpxgen.generate("mixed", n_hits=2_000_000, disorder_ticks=384_000)
+    _assert_parity(tpx, h, 320, ctx="J=600us")
+
+
+def test_coord_range_error(tpx):
+    h = tpxgen.generate("tiny")
+    h["x"][123] = 256
+    with pytest.raises(tpx.TpxError) as e:
+        _gpu(tpx, h, 128)
+    assert e.value.status == -3
+    h = tpxgen.generate("tiny")
+    h["toa"][5] = np.uint64(1 << 48)
+    with pytest.raises(tpx.TpxError) as e:
+        _gpu(tpx, h, 128)
+    assert e.value.status == -3
+
+
+def test_capacity_too_small(tpx):
+    h = tpxgen.generate("tiny")
+    rl, rf = oracle.cluster(h, 128)
+    c = tpx.Clusterer(128)
+    d = torch.from_numpy(h.view(np.uint8)).cuda()
+    labels, feats, k = c.run(d, capacity=100, check=False)
+    assert k == len(rf)
+    assert np.array_equal(labels.cpu().numpy().view(np.uint32), rl)
+    assert tpx.features_to_numpy(feats).tobytes() == rf[:100].tobytes()
+
+
+def test_deterministic_repeat(tpx):
+    h = tpxgen.generate("heavyion", n_hits=500_000)
+    a = _gpu(tpx, h, 64)
+    b = _gpu(tpx, h, 64)
+    assert np.array_equal(a[0], b[0]) and a[1].tobytes() == b[1].tobytes()
+
+
+def test_permuted_input(tpx):
+    h = tpxgen.generate("mixed", n_hits=300_000)
+    perm = np.random.default_rng(1).permutation(len(h))
+    _assert_parity(tpx, h[perm].copy(), 320, ctx="permuted")
+
+
+def test_run_host_matches_device(tpx):
+    h = tpxgen.generate("mixed", n_hits=1_000_000)
+    rl, rf = oracle.cluster(h, 320)
+    c = tpx.Clusterer(320)
+    hits = torch.from_numpy(h.view(np.uint8)).pin_memory()
+    labels = torch.empty(len(h), dtype=torch.int32).pin_memory()
+    feats = torch.empty((len(h), 64), dtype=torch.uint8).pin_memory()
+    k = c.run_host(hits, labels, feats)
+    assert k == len(rf)
+    assert np.array_equal(labels.numpy().view(np.uint32), rl)
+    assert tpx.features_to_numpy(feats[:k]).tobytes() == rf.tobytes()
+
+
+# ------------------------------------------- full BASELINE size, sampled parity
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["mixed", "heavyion"])
+def test_full_size_sampled(tpx, preset):
+    """configs[2] (200M) / configs[3] (50M) in the launch configuration
+    bench.py times; oracle components computed one by one for a sample of
+    hits, plus properties that hold at any size."""
+    p = tpxgen.PRESETS[preset]
+    h = tpxgen.generate(preset)
+    n = len(h)
+    gl, gf, k, gc, st = _gpu(tpx, h, p["dt_max"])
+    # properties: canonical labels, partition sums, ordering
+    assert (gl <= np.arange(n, dtype=np.uint32)).all()
+    assert np.array_equal(gl[gl], gl)
+    assert int(gf["size"].astype(np.uint64).sum()) == n
+    assert int(gf["tot_sum"].sum()) == int(h["tot"].astype(np.uint64).sum())
+    assert (np.diff(gf["label"].astype(np.int64)) > 0).all()
+    assert k == int((gl == np.arange(n, dtype=np.uint32)).sum())
+    # sampled oracle components
+    s = oracle.ComponentSampler(h, p["dt_max"])
+    rng = np.random.default_rng(17)
+    for seed in rng.integers(0, n, 400).tolist():
+        f = s.component(seed)
+        assert gl[seed] == f["label"]
+        row = gf[np.searchsorted(gf["label"], f["label"])]
+        for name in pins.FEAT_FIELDS:
+            assert int(row[name]) == int(f[name]), (seed, name)
+    s.close()
