@@ -97,7 +97,7 @@ const char* tpx_status_string(int status);
 
 /* Create a context.  dt_max_ticks: Delta t_max in ToA ticks (0 allowed: only
  * equal ToAs connect).  variant: TPX_VARIANT_*.  width/height: sensor size in
- * pixels, 1..65535 (256x256 Timepix3, 448x512 Timepix4).  *out receives the
+ * pixels, 1..32768 (256x256 Timepix3, 448x512 Timepix4).  *out receives the
  * context (host memory owned by the library, freed by tpx_cluster_destroy).
  * Errors: INVALID_ARG, UNSUPPORTED (variant != LOCAL), CUDA. */
 int tpx_cluster_create(uint64_t dt_max_ticks, int variant, uint32_t width,

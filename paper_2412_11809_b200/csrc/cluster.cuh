@@ -24,6 +24,12 @@ __global__ void k_window_union(const srec* __restrict__ rec, uint64_t n, uint64_
   }
 }
 
+__global__ void k_iota(uint32_t* parent, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    parent[i] = (uint32_t)i;
+}
+
 // Flatten: parent[i] = root(i).
 __global__ void k_flatten(uint32_t* parent, uint64_t n) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;

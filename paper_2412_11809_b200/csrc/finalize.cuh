@@ -1,0 +1,133 @@
+// finalize.cuh -- global merge of border-crossing ("open") components and the
+// ordered emission of feature records (A4 across tiles, A5, A6, A7).
+//
+// Only hits of open components take part in the global union-find; for the
+// 40 Mhit/s mixed stream that is a few percent of the hits.
+#pragma once
+#include "common.cuh"
+#include "sort.cuh"
+#include "tile_cc.cuh"
+
+namespace tpx {
+
+constexpr int kListThreads = 256;
+constexpr int kListGrid = 148 * 8;
+
+__device__ __forceinline__ void flag_internal(dev_hdr* hdr) { atomicOr(&hdr->err, 2u); }
+
+// Hits whose forward window left the staged halo: scan the rest of the window
+// in global memory (any j it reaches belongs to an open component).
+__global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __restrict__ S, uint64_t n, uint64_t dt,
+                                                                  const uint32_t* __restrict__ list, dev_hdr* hdr,
+                                                                  uint32_t* parent_g) {
+  const uint64_t cnt = hdr->n_overflow;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = list[t];
+    const srec a = load_srec(S + i);
+    const uint64_t ta = srec_toa(a);
+    for (uint64_t j = (uint64_t)i + 1; j < n; ++j) {
+      const srec b = load_srec(S + j);
+      if (srec_toa(b) - ta > dt) break;
+      if (adjacent(a.xy, b.xy)) {
+        if (ld_cg(parent_g + j) == kSentinel) {
+          flag_internal(hdr);
+          return;
+        }
+        uf_unite(parent_g, i, (uint32_t)j);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kListThreads) k_pair_unions(const uint2* __restrict__ pairs, dev_hdr* hdr,
+                                                              uint32_t* parent_g) {
+  const uint64_t cnt = hdr->n_pairs;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 p = pairs[t];
+    if (ld_cg(parent_g + p.x) == kSentinel || ld_cg(parent_g + p.y) == kSentinel) {
+      flag_internal(hdr);
+      return;
+    }
+    uf_unite(parent_g, p.x, p.y);
+  }
+}
+
+// Fold every open component's partial record into its final root's record.
+__global__ void __launch_bounds__(kListThreads) k_merge_open(const uint32_t* __restrict__ open_comps, dev_hdr* hdr,
+                                                             const uint32_t* __restrict__ parent_g,
+                                                             const uint32_t* __restrict__ slot_of,
+                                                             tpx_cluster_features* stage) {
+  const uint64_t cnt = hdr->n_open_comps;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = open_comps[t];
+    const uint32_t R = uf_root(parent_g, r);
+    if (R == r) continue;
+    tpx_cluster_features* src = stage + slot_of[r];
+    tpx_cluster_features* dst = stage + slot_of[R];
+    const tpx_cluster_features f = *src;
+    atomicMin(&dst->label, f.label);
+    atomicAdd(&dst->size, f.size);
+    atomicMin((unsigned long long*)&dst->toa_min, (unsigned long long)f.toa_min);
+    atomicMax((unsigned long long*)&dst->toa_max, (unsigned long long)f.toa_max);
+    atomicAdd((unsigned long long*)&dst->tot_sum, (unsigned long long)f.tot_sum);
+    atomicAdd((unsigned long long*)&dst->sum_x, (unsigned long long)f.sum_x);
+    atomicAdd((unsigned long long*)&dst->sum_y, (unsigned long long)f.sum_y);
+    atomicAdd((unsigned long long*)&dst->sum_tot_x, (unsigned long long)f.sum_tot_x);
+    atomicAdd((unsigned long long*)&dst->sum_tot_y, (unsigned long long)f.sum_tot_y);
+    src->size = 0;  // merged away: k_emit skips it
+  }
+}
+
+// Labels of open hits; label bits of open final roots.
+__global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __restrict__ S,
+                                                              const uint32_t* __restrict__ open_hits,
+                                                              const uint32_t* __restrict__ open_comps, dev_hdr* hdr,
+                                                              const uint32_t* __restrict__ parent_g,
+                                                              const uint32_t* __restrict__ slot_of,
+                                                              const tpx_cluster_features* __restrict__ stage,
+                                                              uint32_t* __restrict__ labels, uint32_t* bitmap) {
+  const uint64_t nh = hdr->n_open_hits, nc = hdr->n_open_comps;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh; t += stride) {
+    const uint32_t pos = open_hits[t];
+    const uint32_t R = uf_root(parent_g, pos);
+    labels[S[pos].idx] = stage[slot_of[R]].label;
+  }
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += stride) {
+    const uint32_t r = open_comps[t];
+    if (uf_root(parent_g, r) == r) set_label_bit(bitmap, stage[slot_of[r]].label);
+  }
+}
+
+__global__ void k_popc(const uint32_t* __restrict__ bitmap, uint64_t nwords, uint32_t* __restrict__ cnt) {
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (uint64_t)gridDim.x * blockDim.x)
+    cnt[w] = __popc(bitmap[w]);
+}
+
+// A6 + A7: ordinal of a label = set bits below it in the label bitmap; copy
+// the staged record to features_out[ordinal] (ascending label order).
+__global__ void __launch_bounds__(256) k_emit(const tpx_cluster_features* __restrict__ stage,
+                                              const uint32_t* __restrict__ comp_count,
+                                              const uint32_t* __restrict__ bitmap,
+                                              const uint32_t* __restrict__ wbase,
+                                              tpx_cluster_features* __restrict__ out, uint64_t capacity) {
+  const uint32_t cc = comp_count[blockIdx.x];
+  const uint64_t t0 = (uint64_t)blockIdx.x * kTile;
+  for (uint32_t c = threadIdx.x; c < cc; c += blockDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(stage + t0 + c);
+    const uint4 q0 = __ldcs(src);
+    const uint32_t size = q0.y;
+    if (size == 0) continue;
+    const uint32_t label = q0.x;
+    const uint32_t w = label >> 5;
+    const uint64_t ord = (uint64_t)wbase[w] + __popc(bitmap[w] & ((1u << (label & 31)) - 1u));
+    if (ord >= capacity) continue;
+    uint4* dst = reinterpret_cast<uint4*>(out + ord);
+    dst[0] = q0;
+    dst[1] = __ldcs(src + 1);
+    dst[2] = __ldcs(src + 2);
+    dst[3] = __ldcs(src + 3);
+  }
+}
+
+}  // namespace tpx

@@ -11,12 +11,16 @@ namespace tpx {
 struct dev_hdr {
   unsigned long long toa_min;
   unsigned long long toa_max;
-  unsigned int err;          // bit 0: coordinate / ToA range violation
+  unsigned int err;          // bit 0: coordinate / ToA range violation; bit 1: internal
   unsigned int sort_bad;     // windowed-sort verification failures
   unsigned long long n_clusters;
-  unsigned long long n_pairs;
-  unsigned long long pad[3];
+  unsigned long long n_pairs;       // cross-tile union pairs
+  unsigned long long n_open_comps;  // components touching a tile border
+  unsigned long long n_open_hits;   // hits of those components
+  unsigned long long n_overflow;    // hits whose window left the staged halo
+  unsigned long long pad[8];
 };
+static_assert(sizeof(dev_hdr) == 128, "dev_hdr layout");
 
 constexpr int kMMThreads = 256;
 

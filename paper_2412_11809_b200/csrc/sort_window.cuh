@@ -1,0 +1,219 @@
+// sort_window.cuh -- bounded-disorder ToA sort (A2), one pass over HBM.
+//
+// The input is t-ordered (§3.1 l.99-100): hits arrive almost in ToA
+// order.  If no hit is displaced by more than D positions from its place in
+// the (toa, input index) order, the hits that land in output positions
+// [kT, (k+1)T) all come from input window [kT-D, (k+1)T+D), and exactly the
+// first kT-ws of that window (ws = max(0, kT-D)) precede them.  So CTA k
+// loads the window, sorts it in shared memory with a stable LSD radix sort on
+// toa - window_min (ties keep input order => (toa, index) order), and writes
+// the middle T records.  Whether D held is verified afterwards: the
+// concatenation is correct iff it is strictly increasing in (toa, index)
+// across CTA borders (k_tile_cc checks every border); otherwise the host
+// retries with a larger D and finally with the global radix sort (sort.cuh).
+// Fused: coordinate / ToA-range validation of every hit.
+#pragma once
+#include "common.cuh"
+#include "sort.cuh"
+
+namespace tpx {
+
+constexpr int kWSortThreads = 512;
+constexpr int kWSortWarps = kWSortThreads / 32;
+constexpr int kWSortTile = 4096;   // output records per CTA (T)
+
+template <int IT>
+struct wsort_cfg {
+  static constexpr int W = kWSortThreads * IT;         // window capacity
+  static constexpr int D = (W - kWSortTile) / 2;       // displacement bound
+  static constexpr int PER_WARP = IT * 32;
+};
+
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* sm) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  if (lane_id() == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long x = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : ~0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = min(x, __shfl_xor_sync(kFull, x, o));
+    if (threadIdx.x == 0) sm[32] = x;
+  }
+  __syncthreads();
+  unsigned long long r = sm[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v, unsigned long long* sm) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  if (lane_id() == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long x = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(kFull, x, o));
+    if (threadIdx.x == 0) sm[32] = x;
+  }
+  __syncthreads();
+  unsigned long long r = sm[32];
+  __syncthreads();
+  return r;
+}
+
+template <int IT>
+__global__ void __launch_bounds__(kWSortThreads, 1) k_window_sort(const tpx_hit* __restrict__ hits, uint64_t n,
+                                                                   uint32_t width, uint32_t height,
+                                                                   srec* __restrict__ out, dev_hdr* hdr) {
+  using C = wsort_cfg<IT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);                       // [W]
+  uint16_t* sval = reinterpret_cast<uint16_t*>(skey + C::W);                     // [W]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sval + C::W);                      // [256 * warps]
+  __shared__ unsigned long long red[33];
+
+  const uint64_t k0 = (uint64_t)blockIdx.x * kWSortTile;
+  const uint64_t ws = k0 > (uint64_t)C::D ? k0 - C::D : 0;
+  const uint64_t we = min(n, k0 + kWSortTile + C::D);
+  const uint32_t m = (uint32_t)(we - ws);
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+  // ---- load the window (warp-blocked: warp w owns positions [w*PER_WARP, ...))
+  uint64_t toa[IT];
+  unsigned long long mn = ~0ull, mx = 0;
+  unsigned bad = 0;
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+    toa[r] = 0;
+    if (p < m) {
+      hit4 h = load_hit(hits + ws + p);
+      toa[r] = h.toa;
+      mn = min(mn, (unsigned long long)h.toa);
+      mx = max(mx, (unsigned long long)h.toa);
+      bad |= (h.x >= width) | (h.y >= height) | (h.toa >> 48 != 0);
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->err, 1u);
+  const unsigned long long base = block_min_u64(mn, red);
+  const unsigned long long top = block_max_u64(mx, red);
+  const unsigned long long range = top - base;
+  if (range >> 32) {  // window wider than 32 bits of ticks: leave it to the fallback
+    if (threadIdx.x == 0) atomicAdd(&hdr->sort_bad, 1u);
+    return;
+  }
+  const int bits = range ? 64 - __clzll(range) : 0;
+  const int passes = (bits + 7) >> 3;
+  uint32_t key[IT];
+  uint16_t val[IT];
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+    key[r] = (uint32_t)(toa[r] - base);
+    val[r] = (uint16_t)p;
+  }
+
+  // ---- stable LSD radix passes, 8 bits each, ranks via warp-private counters
+  for (int pass = 0; pass < passes || pass == 0; ++pass) {
+    const int shift = pass * 8;
+    for (int i = threadIdx.x; i < 256 * kWSortWarps; i += kWSortThreads) cnt[i] = 0;
+    __syncthreads();
+    uint16_t lr[IT];
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+      const bool valid = p < m;
+      const unsigned d = valid ? (key[r] >> shift) & 0xffu : 256u;
+      const unsigned peers = __match_any_sync(kFull, d);
+      uint32_t b = 0;
+      if (valid) b = cnt[d * kWSortWarps + warp];
+      lr[r] = (uint16_t)(b + __popc(peers & lanemask_lt()));
+      __syncwarp();
+      if (valid && (__ffs(peers) - 1) == (int)lane) cnt[d * kWSortWarps + warp] = b + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // exclusive scan over cnt in (digit, warp) order: 8 consecutive entries per thread
+    {
+      constexpr int PT = 256 * kWSortWarps / kWSortThreads;  // 8
+      uint32_t loc[PT];
+      uint32_t s = 0;
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        loc[i] = cnt[threadIdx.x * PT + i];
+        s += loc[i];
+      }
+      // block exclusive scan of s (512 threads)
+      __shared__ uint32_t wsum[kWSortWarps];
+      uint32_t x = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= (unsigned)o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t t = lane < kWSortWarps ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t y = __shfl_up_sync(kFull, t, o);
+          if (lane >= (unsigned)o) t += y;
+        }
+        if (lane < kWSortWarps) wsum[lane] = t;
+      }
+      __syncthreads();
+      uint32_t ex = (warp ? wsum[warp - 1] : 0) + x - s;
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        cnt[threadIdx.x * PT + i] = ex;
+        ex += loc[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+      if (p < m) {
+        const unsigned d = (key[r] >> shift) & 0xffu;
+        const uint32_t q = cnt[d * kWSortWarps + warp] + lr[r];
+        skey[q] = key[r];
+        sval[q] = val[r];
+      }
+    }
+    __syncthreads();
+    if (pass + 1 < passes) {
+#pragma unroll
+      for (int r = 0; r < IT; ++r) {
+        const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+        if (p < m) {
+          key[r] = skey[p];
+          val[r] = sval[p];
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- write the middle T records (window-local ranks [k0-ws, k0-ws+T))
+  const uint32_t ofs = (uint32_t)(k0 - ws);
+  const uint32_t cnt_out = (uint32_t)min((uint64_t)kWSortTile, n - k0);
+  for (uint32_t j = threadIdx.x; j < cnt_out; j += kWSortThreads) {
+    const uint64_t gi = ws + sval[ofs + j];
+    hit4 h = load_hit(hits + gi);
+    srec r;
+    r.tt = (h.toa << 16) | h.tot;
+    r.xy = (h.y << 16) | h.x;
+    r.idx = (uint32_t)gi;
+    store_srec(out + k0 + j, r);
+  }
+}
+
+template <int IT>
+constexpr size_t window_sort_smem() {
+  return (size_t)wsort_cfg<IT>::W * 6 + 256 * kWSortWarps * 4;
+}
+
+}  // namespace tpx

@@ -1,29 +1,45 @@
 // tpx_cluster.cu -- the C ABI (include/tpx_cluster.h) over the sm_100a kernels.
+//
+// Fast path per run (one host synchronisation, at the end):
+//   k_window_sort      bounded-disorder ToA sort            (sort_window.cuh)
+//   k_tile_cc          tile-local window search + union-find, labels and
+//                      features of tile-closed components  (tile_cc.cuh)
+//   k_overflow_unions, k_pair_unions, k_merge_open, k_open_labels
+//                      global merge of border-crossing components
+//   k_popc + scan + k_emit
+//                      ordinals by label, ordered feature records (finalize.cuh)
+// Fallbacks (taken only when the fast path reports it cannot be exact):
+//   wider sort window -> global LSD radix sort (sort.cuh) -> global
+//   union-find pipeline (cluster.cuh).
 #include <cstdio>
 #include <cstring>
 #include <new>
 
 #include "cluster.cuh"
 #include "common.cuh"
+#include "finalize.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
+#include "sort_window.cuh"
+#include "tile_cc.cuh"
 
 using namespace tpx;
 
 namespace {
 
 constexpr int kMaxStages = 16;
-const char* const kStageNames[kMaxStages] = {
-    "validate", "sort", "gather", "union", "flatten", "labels", "compact", "features",
-    "", "", "", "", "", "", "", ""};
+const char* const kStageNames[kMaxStages] = {"sort", "tile_cc", "border_merge", "emit", "", "", "", "",
+                                             "",     "",        "",             "",     "", "", "", ""};
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+uint32_t n_tiles_of(uint64_t n, int tile) { return (uint32_t)((n + tile - 1) / tile); }
 
 struct layout {
-  size_t hdr, keys0, keys1, vals0, vals1, rec, parent, minidx, flags, ord, hist, partials, total;
+  size_t hdr, S, parent, slot_of, stage, comp_count, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
+  size_t keys0, keys1, vals0, vals1, hist, minidx, flags, ord;
+  size_t total;
+  uint32_t tiles, nwords;
 };
-
-uint32_t n_tiles_of(uint64_t n, int tile) { return (uint32_t)((n + tile - 1) / tile); }
 
 layout make_layout(uint64_t n) {
   layout L;
@@ -33,21 +49,33 @@ layout make_layout(uint64_t n) {
     off += align256(bytes);
     return o;
   };
+  L.tiles = n_tiles_of(n, kTile);
+  L.nwords = (uint32_t)((n + 31) / 32);
   const uint32_t rt = n_tiles_of(n, kRadixTile);
-  const uint32_t st_hist = n_tiles_of((uint64_t)rt * kRadixBins, kScanTile);
-  const uint32_t st_n = n_tiles_of(n, kScanTile);
+  uint32_t st = n_tiles_of((uint64_t)rt * kRadixBins, kScanTile);
+  st = st > n_tiles_of(n, kScanTile) ? st : n_tiles_of(n, kScanTile);
   L.hdr = take(sizeof(dev_hdr));
+  L.S = take(n * 16);
+  L.parent = take(n * 4);
+  L.slot_of = take(n * 4);
+  L.stage = take((size_t)L.tiles * kTile * 64);
+  L.comp_count = take((size_t)L.tiles * 4);
+  L.open_hits = take(n * 4);
+  L.open_comps = take(n * 4);
+  L.overflow = take(n * 4);
+  L.pairs = take(n * 8);
+  L.bitmap = take((size_t)L.nwords * 4);
+  L.wcnt = take((size_t)L.nwords * 4);
+  L.partials = take((size_t)st * 4 + 4);
+  // fallback-only buffers
   L.keys0 = take(n * 8);
   L.keys1 = take(n * 8);
   L.vals0 = take(n * 4);
   L.vals1 = take(n * 4);
-  L.rec = take(n * 16);
-  L.parent = take(n * 4);
+  L.hist = take((size_t)rt * kRadixBins * 4);
   L.minidx = take(n * 4);
   L.flags = take(n * 4);
   L.ord = take(n * 4);
-  L.hist = take((size_t)rt * kRadixBins * 4);
-  L.partials = take((size_t)(st_hist > st_n ? st_hist : st_n) * 4 + 4);
   L.total = off;
   return L;
 }
@@ -65,10 +93,35 @@ struct tpx_cluster {
   int cuda_ready;  // CUDA resources are created lazily by the first run
 };
 
-// Pinned header + timing events, created on first use so that contexts can be
-// created (and arguments validated) on a machine without a GPU.
+#define TPX_CUDA(call)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      fprintf(stderr, "tpx_cluster: %s failed: %s\n", #call, cudaGetErrorString(e_)); \
+      return TPX_ERR_CUDA;                                                             \
+    }                                                                                  \
+  } while (0)
+
+#define TPX_LAUNCHED(ctx)                                                          \
+  do {                                                                             \
+    (ctx)->stats.kernel_launches++;                                                \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess) {                                                       \
+      fprintf(stderr, "tpx_cluster: launch failed: %s\n", cudaGetErrorString(e_)); \
+      return TPX_ERR_CUDA;                                                         \
+    }                                                                              \
+  } while (0)
+
+// Pinned header + timing events + kernel attributes, created on first use so
+// that contexts can be created (and arguments validated) without a GPU.
 static int ensure_cuda(tpx_cluster* c) {
   if (c->cuda_ready) return TPX_OK;
+  if (cudaFuncSetAttribute(k_window_sort<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)window_sort_smem<12>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_window_sort<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)window_sort_smem<24>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tile_cc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess)
+    return TPX_ERR_CUDA;
   if (cudaMallocHost(&c->host_hdr, sizeof(dev_hdr)) != cudaSuccess) return TPX_ERR_CUDA;
   for (int i = 0; i <= kMaxStages; ++i) {
     if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
@@ -80,25 +133,6 @@ static int ensure_cuda(tpx_cluster* c) {
   c->cuda_ready = 1;
   return TPX_OK;
 }
-
-#define TPX_CUDA(call)                                                                   \
-  do {                                                                                   \
-    cudaError_t e_ = (call);                                                             \
-    if (e_ != cudaSuccess) {                                                             \
-      fprintf(stderr, "tpx_cluster: %s failed: %s\n", #call, cudaGetErrorString(e_));   \
-      return TPX_ERR_CUDA;                                                               \
-    }                                                                                    \
-  } while (0)
-
-#define TPX_LAUNCHED(ctx)                                                                \
-  do {                                                                                   \
-    (ctx)->stats.kernel_launches++;                                                      \
-    cudaError_t e_ = cudaGetLastError();                                                 \
-    if (e_ != cudaSuccess) {                                                             \
-      fprintf(stderr, "tpx_cluster: launch failed: %s\n", cudaGetErrorString(e_));       \
-      return TPX_ERR_CUDA;                                                               \
-    }                                                                                    \
-  } while (0)
 
 static int grid_for(uint64_t n, int threads) {
   uint64_t g = (n + threads - 1) / threads;
@@ -147,10 +181,170 @@ static int radix_sort(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t 
                                                                    k1, v1);
     }
     TPX_LAUNCHED(c);
-    KeyT* tk = k0; k0 = k1; k1 = tk;
-    uint32_t* tv = v0; v0 = v1; v1 = tv;
+    KeyT* tk = k0;
+    k0 = k1;
+    k1 = tk;
+    uint32_t* tv = v0;
+    v0 = v1;
+    v1 = tv;
   }
   *perm_out = passes ? v0 : nullptr;
+  return TPX_OK;
+}
+
+struct run_ptrs {
+  const tpx_hit* hits;
+  uint64_t n;
+  uint32_t* labels;
+  tpx_cluster_features* feats;
+  uint64_t capacity;
+  char* ws;
+  layout L;
+  cudaStream_t s;
+};
+
+static int reset_header(tpx_cluster* c, const run_ptrs& r) {
+  dev_hdr init;
+  memset(&init, 0, sizeof(init));
+  init.toa_min = ~0ull;
+  TPX_CUDA(cudaMemcpyAsync(r.ws + r.L.hdr, &init, sizeof(init), cudaMemcpyHostToDevice, r.s));
+  TPX_CUDA(cudaMemsetAsync(r.ws + r.L.bitmap, 0, (size_t)r.L.nwords * 4, r.s));
+  (void)c;
+  return TPX_OK;
+}
+
+static int read_header(tpx_cluster* c, const run_ptrs& r) {
+  TPX_CUDA(cudaMemcpyAsync(c->host_hdr, r.ws + r.L.hdr, sizeof(dev_hdr), cudaMemcpyDeviceToHost, r.s));
+  TPX_CUDA(cudaStreamSynchronize(r.s));
+  return TPX_OK;
+}
+
+// Global LSD radix sort into S (fallback when the windowed sort cannot prove
+// its displacement bound).  Needs the ToA range first: one extra host sync.
+static int sort_global(tpx_cluster* c, const run_ptrs& r) {
+  dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
+  const int g = grid_for(r.n, kMMThreads) < 148 * 8 ? grid_for(r.n, kMMThreads) : 148 * 8;
+  k_validate_minmax<<<g, kMMThreads, 0, r.s>>>(r.hits, r.n, c->width, c->height, hdr);
+  TPX_LAUNCHED(c);
+  int rc = read_header(c, r);
+  if (rc) return rc;
+  if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
+  const uint64_t toa_min = c->host_hdr->toa_min, range = c->host_hdr->toa_max - toa_min;
+  const int bits = range ? 64 - __builtin_clzll(range) : 0;
+  const int passes = (bits + 7) / 8;
+  uint32_t* perm = nullptr;
+  rc = (bits <= 32) ? radix_sort<uint32_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s)
+                    : radix_sort<uint64_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s);
+  if (rc) return rc;
+  k_gather_init<<<grid_for(r.n, 256), 256, 0, r.s>>>(r.hits, perm, r.n, (srec*)(r.ws + r.L.S),
+                                                     (uint32_t*)(r.ws + r.L.parent));
+  TPX_LAUNCHED(c);
+  return TPX_OK;
+}
+
+// Tile clustering + border merge + ordered emission on a sorted S.
+static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
+  char* ws = r.ws;
+  const layout& L = r.L;
+  dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
+  const srec* S = (const srec*)(ws + L.S);
+  uint32_t* parent_g = (uint32_t*)(ws + L.parent);
+  uint32_t* slot_of = (uint32_t*)(ws + L.slot_of);
+  tpx_cluster_features* stage = (tpx_cluster_features*)(ws + L.stage);
+  uint32_t* comp_count = (uint32_t*)(ws + L.comp_count);
+  uint32_t* open_hits = (uint32_t*)(ws + L.open_hits);
+  uint32_t* open_comps = (uint32_t*)(ws + L.open_comps);
+  uint32_t* overflow = (uint32_t*)(ws + L.overflow);
+  uint2* pairs = (uint2*)(ws + L.pairs);
+  uint32_t* bitmap = (uint32_t*)(ws + L.bitmap);
+  uint32_t* wcnt = (uint32_t*)(ws + L.wcnt);
+  uint32_t* partials = (uint32_t*)(ws + L.partials);
+
+  if (c->profiling) cudaEventRecord(c->ev[1], r.s);
+  tile_args a;
+  a.S = S;
+  a.n = r.n;
+  a.dt = c->dt;
+  a.width = c->width;
+  a.bucket_shift = 0;
+  while (((c->width - 1) >> a.bucket_shift) >= (uint32_t)kBuckets) ++a.bucket_shift;
+  a.labels = r.labels;
+  a.parent_g = parent_g;
+  a.slot_of = slot_of;
+  a.stage = stage;
+  a.comp_count = comp_count;
+  a.bitmap = bitmap;
+  a.open_hits = open_hits;
+  a.open_comps = open_comps;
+  a.pairs = pairs;
+  a.overflow = overflow;
+  a.hdr = hdr;
+  a.verify_stride = kWSortTile;
+  k_tile_cc<<<L.tiles, kTileThreads, kTileSmem, r.s>>>(a);
+  TPX_LAUNCHED(c);
+
+  if (c->profiling) cudaEventRecord(c->ev[2], r.s);
+  k_overflow_unions<<<kListGrid, kListThreads, 0, r.s>>>(S, r.n, c->dt, overflow, hdr, parent_g);
+  TPX_LAUNCHED(c);
+  k_pair_unions<<<kListGrid, kListThreads, 0, r.s>>>(pairs, hdr, parent_g);
+  TPX_LAUNCHED(c);
+  k_merge_open<<<kListGrid, kListThreads, 0, r.s>>>(open_comps, hdr, parent_g, slot_of, stage);
+  TPX_LAUNCHED(c);
+  k_open_labels<<<kListGrid, kListThreads, 0, r.s>>>(S, open_hits, open_comps, hdr, parent_g, slot_of, stage,
+                                                     r.labels, bitmap);
+  TPX_LAUNCHED(c);
+
+  if (c->profiling) cudaEventRecord(c->ev[3], r.s);
+  k_popc<<<grid_for(L.nwords, 256), 256, 0, r.s>>>(bitmap, L.nwords, wcnt);
+  TPX_LAUNCHED(c);
+  int rc = exclusive_scan(c, wcnt, L.nwords, wcnt, partials, (uint32_t*)&hdr->n_clusters, r.s);
+  if (rc) return rc;
+  if (r.capacity) {
+    k_emit<<<L.tiles, 256, 0, r.s>>>(stage, comp_count, bitmap, wcnt, r.feats, r.capacity);
+    TPX_LAUNCHED(c);
+  }
+  if (c->profiling) cudaEventRecord(c->ev[4], r.s);
+  return TPX_OK;
+}
+
+// Global union-find pipeline (cluster.cuh) on a sorted S -- the internal
+// fallback if the tile path ever reports an inconsistency.
+static int cluster_global(tpx_cluster* c, const run_ptrs& r) {
+  char* ws = r.ws;
+  const layout& L = r.L;
+  dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
+  const srec* S = (const srec*)(ws + L.S);
+  uint32_t* parent = (uint32_t*)(ws + L.parent);
+  uint32_t* minidx = (uint32_t*)(ws + L.minidx);
+  uint32_t* flags = (uint32_t*)(ws + L.flags);
+  uint32_t* ord = (uint32_t*)(ws + L.ord);
+  uint32_t* partials = (uint32_t*)(ws + L.partials);
+  const uint64_t n = r.n;
+  if (c->profiling) cudaEventRecord(c->ev[1], r.s);
+  k_iota<<<grid_for(n, 256), 256, 0, r.s>>>(parent, n);
+  TPX_LAUNCHED(c);
+  k_window_union<<<grid_for(n, 256), 256, 0, r.s>>>(S, n, c->dt, parent);
+  TPX_LAUNCHED(c);
+  k_flatten<<<grid_for(n, 256), 256, 0, r.s>>>(parent, n);
+  TPX_LAUNCHED(c);
+  if (c->profiling) cudaEventRecord(c->ev[2], r.s);
+  TPX_CUDA(cudaMemsetAsync(minidx, 0xff, n * 4, r.s));
+  k_minidx<<<grid_for(n, 256), 256, 0, r.s>>>(S, parent, n, minidx);
+  TPX_LAUNCHED(c);
+  k_labels<<<grid_for(n, 256), 256, 0, r.s>>>(S, parent, minidx, n, r.labels);
+  TPX_LAUNCHED(c);
+  k_flags<<<grid_for(n, 256), 256, 0, r.s>>>(r.labels, n, flags);
+  TPX_LAUNCHED(c);
+  if (c->profiling) cudaEventRecord(c->ev[3], r.s);
+  int rc = exclusive_scan(c, flags, n, ord, partials, (uint32_t*)&hdr->n_clusters, r.s);
+  if (rc) return rc;
+  if (r.capacity) {
+    k_feat_init<<<grid_for(n, 256), 256, 0, r.s>>>(r.labels, ord, n, r.feats, r.capacity);
+    TPX_LAUNCHED(c);
+    k_feat_accum<<<grid_for(n, 256), 256, 0, r.s>>>(S, parent, minidx, ord, n, r.feats, r.capacity);
+    TPX_LAUNCHED(c);
+  }
+  if (c->profiling) cudaEventRecord(c->ev[4], r.s);
   return TPX_OK;
 }
 
@@ -179,7 +373,7 @@ int tpx_cluster_create(uint64_t dt_max_ticks, int variant, uint32_t width, uint3
   if (!out) return TPX_ERR_INVALID_ARG;
   *out = nullptr;
   if (variant < TPX_VARIANT_LOCAL || variant > TPX_VARIANT_STATIC) return TPX_ERR_INVALID_ARG;
-  if (width == 0 || height == 0 || width > 65535 || height > 65535) return TPX_ERR_INVALID_ARG;
+  if (width == 0 || height == 0 || width > 32768 || height > 32768) return TPX_ERR_INVALID_ARG;
   if (dt_max_ticks >= (1ull << 48)) return TPX_ERR_INVALID_ARG;
   if (variant != TPX_VARIANT_LOCAL) return TPX_ERR_UNSUPPORTED;
   tpx_cluster* c = new (std::nothrow) tpx_cluster;
@@ -234,95 +428,65 @@ int tpx_cluster_run(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* l
   if (((uintptr_t)hits & 15) || ((uintptr_t)workspace & 255) || ((uintptr_t)features_out & 15) ||
       ((uintptr_t)labels_out & 3))
     return TPX_ERR_INVALID_ARG;
-  const layout L = make_layout(n);
-  if (workspace_bytes < L.total) return TPX_ERR_OOM;
+  run_ptrs r;
+  r.L = make_layout(n);
+  if (workspace_bytes < r.L.total) return TPX_ERR_OOM;
   if (ensure_cuda(c)) return TPX_ERR_CUDA;
-  cudaStream_t s = (cudaStream_t)stream;
-  char* ws = (char*)workspace;
-  dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
-  srec* rec = (srec*)(ws + L.rec);
-  uint32_t* parent = (uint32_t*)(ws + L.parent);
-  uint32_t* minidx = (uint32_t*)(ws + L.minidx);
-  uint32_t* flags = (uint32_t*)(ws + L.flags);
-  uint32_t* ord = (uint32_t*)(ws + L.ord);
-  uint32_t* partials = (uint32_t*)(ws + L.partials);
-  int st = 0;
-  auto mark = [&](int stage) {
-    if (c->profiling) {
-      cudaEventRecord(c->ev[stage], s);
-      st = stage;
+  r.hits = hits;
+  r.n = n;
+  r.labels = labels_out;
+  r.feats = features_out;
+  r.capacity = capacity;
+  r.ws = (char*)workspace;
+  r.s = (cudaStream_t)stream;
+  srec* S = (srec*)(r.ws + r.L.S);
+  dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
+  const uint32_t sort_tiles = n_tiles_of(n, kWSortTile);
+
+  int rc;
+  // attempt 0: D = 1024, attempt 1: D = 4096, attempt 2: global radix sort;
+  // attempt 3: global union-find pipeline (internal fallback)
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if ((rc = reset_header(c, r))) return rc;
+    if (c->profiling) cudaEventRecord(c->ev[0], r.s);
+    if (attempt == 0) {
+      k_window_sort<12><<<sort_tiles, kWSortThreads, window_sort_smem<12>(), r.s>>>(hits, n, c->width, c->height, S,
+                                                                                   hdr);
+      TPX_LAUNCHED(c);
+    } else if (attempt == 1) {
+      k_window_sort<24><<<sort_tiles, kWSortThreads, window_sort_smem<24>(), r.s>>>(hits, n, c->width, c->height, S,
+                                                                                   hdr);
+      TPX_LAUNCHED(c);
+    } else {
+      if ((rc = sort_global(c, r))) return rc;
     }
-  };
-
-  // ---- A2 validate + min/max ToA
-  mark(0);
-  dev_hdr init;
-  memset(&init, 0, sizeof(init));
-  init.toa_min = ~0ull;
-  TPX_CUDA(cudaMemcpyAsync(hdr, &init, sizeof(init), cudaMemcpyHostToDevice, s));
-  k_validate_minmax<<<grid_for(n, kMMThreads) < 148 * 8 ? grid_for(n, kMMThreads) : 148 * 8, kMMThreads, 0, s>>>(
-      hits, n, c->width, c->height, hdr);
-  TPX_LAUNCHED(c);
-  TPX_CUDA(cudaMemcpyAsync(c->host_hdr, hdr, sizeof(dev_hdr), cudaMemcpyDeviceToHost, s));
-  TPX_CUDA(cudaStreamSynchronize(s));
-  if (c->host_hdr->err) return TPX_ERR_COORD_RANGE;
-  const uint64_t toa_min = c->host_hdr->toa_min, range = c->host_hdr->toa_max - toa_min;
-  const int bits = range ? 64 - __builtin_clzll(range) : 0;
-  const int passes = (bits + 7) / 8;
-
-  // ---- A2 ToA sort (stable LSD radix on toa - min, payload = input index)
-  mark(1);
-  uint32_t* perm = nullptr;
-  int rc = (bits <= 32) ? radix_sort<uint32_t>(c, hits, n, toa_min, passes, ws, L, &perm, s)
-                        : radix_sort<uint64_t>(c, hits, n, toa_min, passes, ws, L, &perm, s);
-  if (rc) return rc;
-  c->stats.sort_path = 1;
-  mark(2);
-  k_gather_init<<<grid_for(n, 256), 256, 0, s>>>(hits, perm, n, rec, parent);
-  TPX_LAUNCHED(c);
-
-  // ---- A3 + A4 window search + union-find
-  mark(3);
-  k_window_union<<<grid_for(n, 256), 256, 0, s>>>(rec, n, c->dt, parent);
-  TPX_LAUNCHED(c);
-  mark(4);
-  k_flatten<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
-  TPX_LAUNCHED(c);
-
-  // ---- A5 canonical labels
-  mark(5);
-  TPX_CUDA(cudaMemsetAsync(minidx, 0xff, n * 4, s));
-  k_minidx<<<grid_for(n, 256), 256, 0, s>>>(rec, parent, n, minidx);
-  TPX_LAUNCHED(c);
-  k_labels<<<grid_for(n, 256), 256, 0, s>>>(rec, parent, minidx, n, labels_out);
-  TPX_LAUNCHED(c);
-
-  // ---- A6 compaction: ordinal of every label
-  mark(6);
-  k_flags<<<grid_for(n, 256), 256, 0, s>>>(labels_out, n, flags);
-  TPX_LAUNCHED(c);
-  rc = exclusive_scan(c, flags, n, ord, partials, (uint32_t*)&hdr->n_clusters, s);
-  if (rc) return rc;
-
-  // ---- A7 features
-  mark(7);
-  if (capacity) {
-    k_feat_init<<<grid_for(n, 256), 256, 0, s>>>(labels_out, ord, n, features_out, capacity);
-    TPX_LAUNCHED(c);
-    k_feat_accum<<<grid_for(n, 256), 256, 0, s>>>(rec, parent, minidx, ord, n, features_out, capacity);
-    TPX_LAUNCHED(c);
+    c->stats.sort_path = attempt >= 2 ? 1 : 0;
+    c->stats.sort_retries = attempt < 2 ? attempt : 2;
+    rc = attempt == 3 ? cluster_global(c, r) : cluster_sorted(c, r);
+    if (rc) return rc;
+    if ((rc = read_header(c, r))) return rc;
+    const dev_hdr& h = *c->host_hdr;
+    if (h.err & 1u) return TPX_ERR_COORD_RANGE;
+    if (attempt < 2 && h.sort_bad) continue;  // displacement bound violated: widen / fall back
+    if (attempt < 3 && (h.err & 2u)) {        // tile path inconsistency: global pipeline
+      attempt = 2;
+      continue;
+    }
+    break;
   }
-  if (c->profiling) cudaEventRecord(c->ev[8], s);
-  TPX_CUDA(cudaMemcpyAsync(c->host_hdr, hdr, sizeof(dev_hdr), cudaMemcpyDeviceToHost, s));
-  TPX_CUDA(cudaStreamSynchronize(s));
-  const uint64_t k = (uint32_t)c->host_hdr->n_clusters;  // low word written by the scan
+  const dev_hdr& h = *c->host_hdr;
+  const uint64_t k = (uint32_t)h.n_clusters;  // low word written by the scan
   *n_clusters_out = k;
   c->stats.n_clusters = k;
+  c->stats.cross_pairs = h.n_pairs;
   if (c->profiling) {
-    c->stats.n_stages = 8;
-    for (int i = 0; i < 8; ++i) cudaEventElapsedTime(&c->stats.stage_ms[i], c->ev[i], c->ev[i + 1]);
+    c->stats.n_stages = 4;
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]) != cudaSuccess) ms = -1.f;
+      c->stats.stage_ms[i] = ms;
+    }
   }
-  (void)st;
   return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
 }
 

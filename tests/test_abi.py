@@ -57,7 +57,7 @@ def test_abi_version_and_status_strings(lib):
     assert lib.status_string(0) == "ok"
     assert "capacity" in lib.status_string(-5)
     assert lib.status_string(12345) == "unknown status"
-    assert lib.stage_name(1) == "sort" and lib.stage_name(99) == ""
+    assert lib.stage_name(0) == "sort" and lib.stage_name(1) == "tile_cc" and lib.stage_name(99) == ""
 
 
 def test_create_validates_without_gpu(lib):
