@@ -164,6 +164,10 @@ typedef struct tpx_run_stats {
   uint32_t kernel_launches;/* kernels launched by the last run               */
   uint32_t n_stages;       /* valid entries in stage_ms / stage names        */
   float stage_ms[16];      /* per-stage device time (only when profiling)    */
+  uint64_t open_hits;      /* hits of tile-border-crossing components        */
+  uint64_t overflow_hits;  /* hits whose ToA window left the staged halo     */
+  uint64_t tile_phase_cycles[16]; /* tile-kernel phase clocks, summed over
+                              CTAs (only when profiling; diagnostics)        */
 } tpx_run_stats;
 
 int tpx_cluster_last_stats(const tpx_cluster* ctx, tpx_run_stats* out);

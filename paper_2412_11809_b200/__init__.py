@@ -43,6 +43,7 @@ class RunStats(ctypes.Structure):
         ("n_hits", _u64), ("n_clusters", _u64), ("sort_path", _u32), ("sort_retries", _u32),
         ("cross_pairs", _u64), ("kernel_launches", _u32), ("n_stages", _u32),
         ("stage_ms", ctypes.c_float * 16),
+        ("open_hits", _u64), ("overflow_hits", _u64), ("tile_phase_cycles", _u64 * 16),
     ]
 
 
@@ -155,8 +156,9 @@ class Clusterer:
     def stats(self) -> dict:
         s = RunStats()
         _last_stats(self._h, ctypes.byref(s))
-        d = {k: getattr(s, k) for k, _ in RunStats._fields_ if k != "stage_ms"}
+        d = {k: getattr(s, k) for k, _ in RunStats._fields_ if k not in ("stage_ms", "tile_phase_cycles")}
         d["stage_ms"] = {stage_name(i): s.stage_ms[i] for i in range(s.n_stages)}
+        d["tile_phase_cycles"] = list(s.tile_phase_cycles)
         return d
 
     # -- the hot path ------------------------------------------------------

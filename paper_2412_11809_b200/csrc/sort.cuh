@@ -19,8 +19,9 @@ struct dev_hdr {
   unsigned long long n_open_hits;   // hits of those components
   unsigned long long n_overflow;    // hits whose window left the staged halo
   unsigned long long pad[8];
+  unsigned long long phase_cycles[16];  // k_tile_cc per-phase clock totals (profiling)
 };
-static_assert(sizeof(dev_hdr) == 128, "dev_hdr layout");
+static_assert(sizeof(dev_hdr) == 256, "dev_hdr layout");
 
 constexpr int kMMThreads = 256;
 

@@ -30,14 +30,14 @@
 
 namespace tpx {
 
-constexpr int kTileThreads = 512;
-constexpr int kTile = 2048;                    // tile hits per CTA
+constexpr int kTileThreads = 256;
+constexpr int kTile = 1024;                    // tile hits per CTA
 constexpr int kHaloCap = 1024;                 // staged halo hits per side
 constexpr int kFwdMax = kTile + kHaloCap;      // tile + forward halo (local index l)
-constexpr int kBuckets = 4096;                 // column buckets (x >> shift)
+constexpr int kBuckets = 2048;                 // column buckets (x >> shift)
 constexpr int kBucketCap = 512;                // longer buckets: the tile takes the global path
+constexpr int kStageItems = kFwdMax / kTileThreads;        // 8
 constexpr int kItemsPerThread = kTile / kTileThreads;      // 4
-constexpr int kStageItems = kFwdMax / kTileThreads;        // 6
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and chunk
 static_assert(kFwdMax % kTileThreads == 0, "staging layout");
@@ -60,7 +60,17 @@ struct tile_args {
   uint32_t* overflow;        // tile hits whose forward window exceeded the halo
   dev_hdr* hdr;
   uint32_t verify_stride;    // sorted-tile size whose borders are verified
+  unsigned long long* phase_cycles;  // optional per-phase clock totals (profiling), may be null
 };
+
+#define TPX_PHASE(k)                                                         \
+  do {                                                                       \
+    if (a.phase_cycles && threadIdx.x == 0) {                                \
+      const long long now_ = clock64();                                      \
+      atomicAdd(a.phase_cycles + (k), (unsigned long long)(now_ - t_phase)); \
+      t_phase = now_;                                                        \
+    }                                                                        \
+  } while (0)
 
 // |dx| <= 1 and |dy| <= 1 for packed (y << 16 | x) with x, y < 2^15:
 // d = (dy + 1) * 2^16 + (dx + 1) (mod 2^32); the low field is in [0, 2] iff
@@ -99,6 +109,24 @@ __device__ __forceinline__ void s_unite(uint32_t* par, uint32_t a, uint32_t b) {
 
 __device__ __forceinline__ uint64_t srec_key_toa(const srec* S, uint64_t i) { return __ldg(&S[i].tt) >> 16; }
 
+// First p in [lo, hi) with pred(p) (hi if none) for a monotone pred, one warp:
+// 32 probes per round shrink the range 31-fold (3 dependent loads for 1024).
+template <typename Pred>
+__device__ __forceinline__ uint64_t warp_lower_bound(uint64_t lo, uint64_t hi, Pred pred) {
+  const unsigned lane = lane_id();
+  while (hi > lo) {  // invariant: the answer is in [lo, hi], pred(hi) taken as true
+    const uint64_t step = (hi - lo) / 31 + 1;
+    const uint64_t p = lo + lane * step;
+    const bool v = p >= hi ? true : pred(p);
+    const int f = __ffs(__ballot_sync(kFull, v)) - 1;  // lane 31 probes >= hi
+    if (f == 0) return lo;
+    const uint64_t nhi = min(hi, lo + (uint64_t)f * step);
+    lo = lo + (uint64_t)(f - 1) * step + 1;
+    hi = nhi;
+  }
+  return lo;
+}
+
 // Warp-aggregated append of `pred` items to a global list; returns the slot.
 __device__ __forceinline__ uint32_t warp_append(bool pred, unsigned long long* counter) {
   const unsigned m = __ballot_sync(kFull, pred);
@@ -127,57 +155,124 @@ __device__ __forceinline__ void set_label_bit(uint32_t* bitmap, uint32_t label) 
 }
 
 // Shared-memory carve-up (bytes).  Region A holds the column index during the
-// clustering phase and the per-component accumulators afterwards.
+// clustering phase and the staged hits + member array during the reductions.
 struct tile_smem_layout {
-  static constexpr size_t csort = 0;                                  // uint2 [kFwdMax]
-  static constexpr size_t csli = csort + (size_t)kFwdMax * 8;          // u16   [kFwdMax]
-  static constexpr size_t cltmp = csli + (size_t)kFwdMax * 2;          // u16   [kFwdMax]
-  static constexpr size_t myrank = cltmp + (size_t)kFwdMax * 2;        // u16   [kFwdMax]
-  static constexpr size_t region_a = myrank + (size_t)kFwdMax * 2;     // 43008
-  static constexpr size_t hb = region_a;                               // uint2 [kHaloCap]
-  static constexpr size_t bcnt = hb + (size_t)kHaloCap * 8;            // u32   [kBuckets/2 + 1] (u16 pairs)
-  static constexpr size_t par = bcnt + ((size_t)kBuckets / 2 + 4) * 4;  // u32   [kFwdMax]
-  static constexpr size_t csize = par + (size_t)kFwdMax * 4;           // u32   [kTile]
-  static constexpr size_t crank = csize + (size_t)kTile * 4;           // u16   [kTile]
-  static constexpr size_t cacc = crank + (size_t)kTile * 2;            // u16   [kTile]
-  static constexpr size_t eb = cacc + (size_t)kTile * 2;               // u16   [kEdgeBuf * threads]
-  static constexpr size_t copen = eb + (size_t)kEdgeBuf * kTileThreads * 2;  // u8 [kTile]
-  static constexpr size_t hflag = copen + kTile;                       // u8    [kTile]
+  static constexpr size_t csort = 0;                                   // uint2 [kFwdMax]
+  static constexpr size_t csli = csort + (size_t)kFwdMax * 8;           // u16   [kFwdMax]
+  static constexpr size_t myrank = csli + (size_t)kFwdMax * 2;          // u16   [kFwdMax]
+  static constexpr size_t region_a = myrank + (size_t)kFwdMax * 2;
+  // reduction-phase aliases of region A
+  static constexpr size_t stile = 0;                                   // uint4 [kTile]
+  static constexpr size_t mem = stile + (size_t)kTile * 16;             // u16   [kTile]
+  static constexpr size_t big = mem + (size_t)kTile * 2;                // u16   [kTile]
+  static_assert(big + (size_t)kTile * 2 <= region_a, "reduction arrays alias region A");
+  static constexpr size_t hb = region_a;                                // uint2 [kHaloCap] (later: mlabel u32)
+  static constexpr size_t bs = hb + (size_t)kHaloCap * 8;               // u32   [kBuckets + 4]
+  static constexpr size_t par = bs + ((size_t)kBuckets + 4) * 4;        // u32   [kFwdMax]
+  static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile]
+  static constexpr size_t crank = csize + (size_t)kTile * 4;            // u16   [kTile]
+  static constexpr size_t coff = crank + (size_t)kTile * 2;             // u16   [kTile]
+  static constexpr size_t eb = coff + (size_t)kTile * 2;                // u16   [kEdgeBuf * threads]
+  static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2 > (size_t)kFwdMax * 2
+                                         ? (size_t)kEdgeBuf * kTileThreads * 2 : (size_t)kFwdMax * 2;
+  static constexpr size_t cltmp = eb;                                   // u16 [kFwdMax] (alias)
+  static constexpr size_t ccur = eb;                                    // u32 [kTile]   (alias)
+  static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
+  static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
+  static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
   static constexpr size_t total = hflag + kTile;
 };
-static_assert(10 * (kTile / 2) * 4 <= tile_smem_layout::region_a, "accumulators alias region A");
+static_assert((size_t)kTile * 4 <= (size_t)kHaloCap * 8, "mlabel aliases the back halo");
 constexpr size_t kTileSmem = tile_smem_layout::total;
+constexpr uint32_t kBigComp = 24;  // components this large are reduced by a whole warp
 
-__global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
+// Block-wide exclusive scan (kTileThreads threads) of one u32 per thread.
+__device__ __forceinline__ uint32_t tile_block_scan(uint32_t v, uint32_t* total, uint32_t* s_wsum) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t t = lane < kTileThreads / 32 ? s_wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, t, o);
+      if (lane >= (unsigned)o) t += y;
+    }
+    if (lane < kTileThreads / 32) s_wsum[lane] = t;
+  }
+  __syncthreads();
+  *total = s_wsum[kTileThreads / 32 - 1];
+  const uint32_t r = (warp ? s_wsum[warp - 1] : 0) + x - v;
+  __syncthreads();
+  return r;
+}
+
+struct feat_acc {
+  uint32_t tmin, tmax, midx;
+  uint64_t tot, sx, sy, stx, sty;
+  __device__ __forceinline__ void init() {
+    tmin = 0xffffffffu;
+    tmax = 0;
+    midx = 0xffffffffu;
+    tot = sx = sy = stx = sty = 0;
+  }
+  // one staged hit: (toa - base, y<<16|x, tot, input index)
+  __device__ __forceinline__ void add(const uint4 h) {
+    const uint32_t x = h.y & 0xffffu, y = h.y >> 16, t = h.z;
+    tmin = min(tmin, h.x);
+    tmax = max(tmax, h.x);
+    midx = min(midx, h.w);
+    tot += t;
+    sx += x;
+    sy += y;
+    stx += (uint64_t)t * x;
+    sty += (uint64_t)t * y;
+  }
+  __device__ __forceinline__ void warp_reduce() {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      tmin = min(tmin, __shfl_xor_sync(kFull, tmin, o));
+      tmax = max(tmax, __shfl_xor_sync(kFull, tmax, o));
+      midx = min(midx, __shfl_xor_sync(kFull, midx, o));
+      tot += __shfl_xor_sync(kFull, tot, o);
+      sx += __shfl_xor_sync(kFull, sx, o);
+      sy += __shfl_xor_sync(kFull, sy, o);
+      stx += __shfl_xor_sync(kFull, stx, o);
+      sty += __shfl_xor_sync(kFull, sty, o);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
   using SL = tile_smem_layout;
   extern __shared__ __align__(16) unsigned char sm[];
   uint2* csort = reinterpret_cast<uint2*>(sm + SL::csort);      // (toa - base, y<<16|x), bucket-sorted
   uint16_t* csli = reinterpret_cast<uint16_t*>(sm + SL::csli);  // local index of csort entries
-  uint16_t* cltmp = reinterpret_cast<uint16_t*>(sm + SL::cltmp);
   uint16_t* myrank = reinterpret_cast<uint16_t*>(sm + SL::myrank);  // local index -> csort position
+  uint4* stile = reinterpret_cast<uint4*>(sm + SL::stile);      // tile hits (toa - base, xy, tot, idx)
+  uint16_t* mem = reinterpret_cast<uint16_t*>(sm + SL::mem);    // member array grouped by component
+  uint16_t* big = reinterpret_cast<uint16_t*>(sm + SL::big);    // roots of large components
   uint2* hb = reinterpret_cast<uint2*>(sm + SL::hb);            // back halo, index order
-  uint32_t* bcnt = reinterpret_cast<uint32_t*>(sm + SL::bcnt);  // bucket counts / starts, 2 x u16 per word
+  uint32_t* mlabel = reinterpret_cast<uint32_t*>(sm + SL::hb);  // label by tile root (after the search)
+  uint32_t* bs = reinterpret_cast<uint32_t*>(sm + SL::bs);      // bucket counts, then bucket starts
   uint32_t* par = reinterpret_cast<uint32_t*>(sm + SL::par);
   uint32_t* csize = reinterpret_cast<uint32_t*>(sm + SL::csize);
-  uint16_t* crank = reinterpret_cast<uint16_t*>(sm + SL::crank);
-  uint16_t* cacc = reinterpret_cast<uint16_t*>(sm + SL::cacc);
+  uint16_t* crank = reinterpret_cast<uint16_t*>(sm + SL::crank);  // stage rank by root
+  uint16_t* coff = reinterpret_cast<uint16_t*>(sm + SL::coff);    // member offset by root
   uint16_t* eb = reinterpret_cast<uint16_t*>(sm + SL::eb);
+  uint16_t* cltmp = reinterpret_cast<uint16_t*>(sm + SL::cltmp);
+  uint32_t* ccur = reinterpret_cast<uint32_t*>(sm + SL::ccur);
   uint8_t* copen = sm + SL::copen;
   uint8_t* hflag = sm + SL::hflag;  // per tile hit: bit0 open mark, bit1 overflow
-  // accumulators (region A, after clustering)
-  uint32_t* a_tot = reinterpret_cast<uint32_t*>(sm);
-  uint32_t* a_sx = a_tot + kTile / 2;
-  uint32_t* a_sy = a_sx + kTile / 2;
-  uint32_t* a_vxl = a_sy + kTile / 2;  // sum(tot*x) and sum(tot*y) in 16-bit halves
-  uint32_t* a_vxh = a_vxl + kTile / 2;
-  uint32_t* a_vyl = a_vxh + kTile / 2;
-  uint32_t* a_vyh = a_vyl + kTile / 2;
-  uint32_t* a_tmin = a_vyh + kTile / 2;
-  uint32_t* a_tmax = a_tmin + kTile / 2;
-  uint32_t* a_midx = a_tmax + kTile / 2;
   __shared__ uint64_t s_meta[8];
   __shared__ uint32_t s_wsum[kTileThreads / 32];
-  __shared__ uint32_t s_chunk, s_bmax;
+  __shared__ uint32_t s_chunk, s_bmax, s_nbig, s_bigq;
 
   const uint64_t n = a.n, dt = a.dt;
   const srec* __restrict__ S = a.S;
@@ -186,54 +281,56 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
   const uint32_t nt = (uint32_t)(t1 - t0);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t shift = a.bucket_shift;
+  long long t_phase = clock64();
 
-  // ---- halo ranges (binary searches in the sorted stream), sort verification
-  if (threadIdx.x == 0) {
-    const uint64_t toa_first = srec_key_toa(S, t0), toa_last = srec_key_toa(S, t1 - 1);
+  // ---- halo ranges (32-ary warp searches in the sorted stream: warp 0 the
+  // back halo, warp 1 the forward halo), sort verification
+  if (warp == 0) {
+    const uint64_t toa_first = srec_key_toa(S, t0);
     const uint64_t blim = t0 > (uint64_t)kHaloCap ? t0 - kHaloCap : 0;
-    uint64_t lo = blim, hi = t0;  // back halo: first position with toa + dt >= toa_first
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (srec_key_toa(S, mid) + dt < toa_first) lo = mid + 1; else hi = mid;
+    // back halo: first position with toa + dt >= toa_first
+    const uint64_t b0 = warp_lower_bound(blim, t0, [&](uint64_t p) { return srec_key_toa(S, p) + dt >= toa_first; });
+    if (lane == 0) {
+      const bool btrunc = b0 == blim && blim > 0 && srec_key_toa(S, blim - 1) + dt >= toa_first;
+      s_meta[0] = b0;
+      s_meta[2] = srec_key_toa(S, b0);               // base: the smallest staged ToA
+      s_meta[3] = btrunc ? 1u : 0u;
+      s_meta[5] = t0 ? srec_key_toa(S, t0 - 1) : 0;  // ToA of the previous tile's last hit
+      s_chunk = 0;
+      s_bmax = 0;
+      s_nbig = 0;
+      s_bigq = 0;
     }
-    const uint64_t b0 = lo;
-    const bool btrunc = b0 == blim && blim > 0 && srec_key_toa(S, blim - 1) + dt >= toa_first;
+  } else if (warp == 1) {
+    const uint64_t toa_last = srec_key_toa(S, t1 - 1);
     const uint64_t flim = min(n, t1 + kHaloCap);
-    lo = t1;
-    hi = flim;  // forward halo: first position with toa > toa_last + dt
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (srec_key_toa(S, mid) <= toa_last + dt) lo = mid + 1; else hi = mid;
+    // forward halo: first position with toa > toa_last + dt
+    const uint64_t f1 = warp_lower_bound(t1, flim, [&](uint64_t p) { return srec_key_toa(S, p) > toa_last + dt; });
+    if (lane == 0) {
+      const bool ftrunc = f1 == flim && flim < n && srec_key_toa(S, flim) <= toa_last + dt;
+      s_meta[1] = f1;
+      s_meta[4] = ftrunc ? srec_key_toa(S, f1) : 0;  // ToA of the first hit not staged
+      s_meta[6] = srec_key_toa(S, f1 - 1);           // largest staged ToA
+      s_meta[7] = ftrunc ? 2u : 0u;
     }
-    const uint64_t f1 = lo;
-    const bool ftrunc = f1 == flim && flim < n && srec_key_toa(S, flim) <= toa_last + dt;
-    const uint64_t base = srec_key_toa(S, b0);
-    const bool wide = (srec_key_toa(S, f1 - 1) - base) >> 32 != 0;
-    s_meta[0] = b0;
-    s_meta[1] = f1;
-    s_meta[2] = base;
-    s_meta[3] = (btrunc ? 1u : 0u) | (ftrunc ? 2u : 0u) | (wide ? 4u : 0u);
-    s_meta[4] = ftrunc ? srec_key_toa(S, f1) : 0;  // ToA of the first hit not staged
-    s_meta[5] = t0 ? srec_key_toa(S, t0 - 1) : 0;  // ToA of the previous tile's last hit
-    if (t0 > 0 && (t0 % a.verify_stride) == 0) {   // sort verification at sorted-tile borders
-      const srec p = load_srec(S + t0 - 1), q = load_srec(S + t0);
-      const uint64_t tp = srec_toa(p), tq = srec_toa(q);
-      if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&a.hdr->sort_bad, 1u);
-    }
-    s_chunk = 0;
-    s_bmax = 0;
+  } else if (threadIdx.x == 64 && t0 > 0 && (t0 % a.verify_stride) == 0) {
+    // sort verification at sorted-tile borders: strictly increasing (toa, index)
+    const srec p = load_srec(S + t0 - 1), q = load_srec(S + t0);
+    const uint64_t tp = srec_toa(p), tq = srec_toa(q);
+    if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&a.hdr->sort_bad, 1u);
   }
-  for (uint32_t w = threadIdx.x; w < kBuckets / 2 + 4; w += kTileThreads) bcnt[w] = 0;
+  for (uint32_t b = threadIdx.x; b < kBuckets + 4; b += kTileThreads) bs[b] = 0;
   for (uint32_t j = threadIdx.x; j < kTile; j += kTileThreads) {
     csize[j] = 0;
     copen[j] = 0;
     hflag[j] = 0;
   }
   __syncthreads();
+  TPX_PHASE(0);
   const uint64_t b0 = s_meta[0], f1 = s_meta[1], base = s_meta[2];
-  const uint32_t flags = (uint32_t)s_meta[3];
+  const uint32_t flags = (uint32_t)(s_meta[3] | s_meta[7]);
   const bool btrunc = flags & 1u, ftrunc = flags & 2u;
-  bool wide = flags & 4u;
+  bool wide = ((s_meta[6] - base) >> 32) != 0;  // staged ToA span exceeds 32 bits
   const uint32_t nb = (uint32_t)(t0 - b0);
   const uint32_t m = (uint32_t)(f1 - t0);  // tile + forward halo
   const uint32_t nf = m - nt;
@@ -253,60 +350,36 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
       if (l < m) {
         const srec r = load_srec(S + t0 + l);
         ev[q] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-        const uint32_t b = (r.xy & 0xffffu) >> shift;
-        const uint32_t old = atomicAdd(bcnt + (b >> 1), 1u << ((b & 1) * 16));
-        eslot[q] = (old >> ((b & 1) * 16)) & 0xffffu;
+        eslot[q] = atomicAdd(bs + ((r.xy & 0xffffu) >> shift), 1u);
       }
     }
   }
   __syncthreads();
-  // exclusive scan of the bucket counts (in place, u16 pairs), max bucket length
+  // exclusive scan of the bucket counts (in place), longest bucket
   if (!wide) {
-    constexpr int PT = kBuckets / kTileThreads;  // 8 buckets per thread
+    constexpr int PT = kBuckets / kTileThreads;  // buckets per thread
     uint32_t cnts[PT];
     uint32_t s = 0, mx = 0;
 #pragma unroll
     for (int i = 0; i < PT; ++i) {
-      const uint32_t b = threadIdx.x * PT + i;
-      cnts[i] = (bcnt[b >> 1] >> ((b & 1) * 16)) & 0xffffu;
+      cnts[i] = bs[threadIdx.x * PT + i];
       s += cnts[i];
       mx = max(mx, cnts[i]);
     }
-    uint32_t x = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= (unsigned)o) x += y;
-    }
     mx = __reduce_max_sync(kFull, mx);
-    if (lane == 31) s_wsum[warp] = x;
     if (lane == 0) atomicMax(&s_bmax, mx);
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t t = lane < kTileThreads / 32 ? s_wsum[lane] : 0;
+    uint32_t tot;
+    uint32_t ex = tile_block_scan(s, &tot, s_wsum);
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, t, o);
-        if (lane >= (unsigned)o) t += y;
-      }
-      if (lane < kTileThreads / 32) s_wsum[lane] = t;
+    for (int i = 0; i < PT; ++i) {
+      bs[threadIdx.x * PT + i] = ex;
+      ex += cnts[i];
     }
-    __syncthreads();
-    uint32_t ex = (warp ? s_wsum[warp - 1] : 0) + x - s;
-    // write starts back as u16 pairs (each thread owns 8 consecutive buckets = 4 words)
-#pragma unroll
-    for (int i = 0; i < PT; i += 2) {
-      const uint32_t lo16 = ex;
-      const uint32_t hi16 = ex + cnts[i];
-      bcnt[(threadIdx.x * PT + i) >> 1] = lo16 | (hi16 << 16);
-      ex += cnts[i] + cnts[i + 1];
-    }
-    if (threadIdx.x == kTileThreads - 1) bcnt[kBuckets / 2] = m;  // start of the sentinel bucket
+    if (threadIdx.x == 0) bs[kBuckets] = m;
   }
   __syncthreads();
+  TPX_PHASE(1);
   if (s_bmax > (uint32_t)kBucketCap) wide = true;  // degenerate column: global path
-
-  auto bstart = [&](uint32_t b) -> uint32_t { return (bcnt[b >> 1] >> ((b & 1) * 16)) & 0xffffu; };
 
   if (wide) {
     // Every hit becomes its own open component; the global pass does the work.
@@ -336,7 +409,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
 #pragma unroll
   for (int q = 0; q < kStageItems; ++q) {
     const uint32_t l = threadIdx.x + q * kTileThreads;
-    if (l < m) cltmp[bstart((ev[q].y & 0xffffu) >> shift) + eslot[q]] = (uint16_t)l;
+    if (l < m) cltmp[bs[(ev[q].y & 0xffffu) >> shift] + eslot[q]] = (uint16_t)l;
   }
   for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;
   __syncthreads();
@@ -345,7 +418,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     const uint32_t l = threadIdx.x + q * kTileThreads;
     if (l < m) {
       const uint32_t b = (ev[q].y & 0xffffu) >> shift;
-      const uint32_t s0 = bstart(b), s1 = bstart(b + 1);
+      const uint32_t s0 = bs[b], s1 = bs[b + 1];
       uint32_t r = 0;
       for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < l;
       const uint32_t fin = s0 + r;
@@ -355,6 +428,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     }
   }
   __syncthreads();
+  TPX_PHASE(2);
 
   // ---- window search over the 3 neighbouring column buckets (dynamic warp
   // chunks; edges buffered, united after each chunk)
@@ -374,28 +448,37 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
       const uint2 h = csort[pself];
       const uint32_t x = h.y & 0xffffu;
       const uint32_t bl = (x ? x - 1 : x) >> shift, bm = x >> shift, br = (x < wmax ? x + 1 : x) >> shift;
+      uint32_t seen = 0;  // neighbouring pixels (3x3 offsets) that already have their first later hit
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const uint32_t b = c == 0 ? bl : (c == 1 ? bm : br);
         if ((c == 0 && b == bm) || (c == 2 && b == bm) || (c == 2 && b == bl)) continue;
-        uint32_t p, pe = bstart(b + 1);
+        uint32_t p, pe = bs[b + 1];
         if (b == bm) {
           p = pself + 1;
         } else {  // first entry of the bucket with local index > j (entries are time-ordered)
-          uint32_t lo = bstart(b), hi = pe;
+          uint32_t lo = bs[b], hi = pe;
           while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
             if (csli[mid] <= j) lo = mid + 1; else hi = mid;
           }
           p = lo;
         }
+        // Only the first later hit on each neighbouring pixel needs an edge:
+        // later hits on that pixel within the window are within dt of it and
+        // reach it through its own same-pixel edge ("window search").
         for (; p < pe; ++p) {
           const uint2 g = csort[p];
           if (g.x - h.x > dt32) break;
-          if (adjacent(h.y, g.y)) {
-            const uint32_t lj = csli[p];
-            if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
-            else s_unite(par, j, lj);
+          const uint32_t d = g.y - h.y + 0x00010001u;  // (dy+1) << 16 | (dx+1) when adjacent
+          if (((d & 0xffffu) <= 2u) & ((d >> 16) <= 2u)) {
+            const uint32_t bit = 1u << ((d >> 16) * 3 + (d & 0xffffu));
+            if (!(seen & bit)) {
+              seen |= bit;
+              const uint32_t lj = csli[p];
+              if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
+              else s_unite(par, j, lj);
+            }
           }
         }
       }
@@ -421,6 +504,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     __syncwarp();
   }
   __syncthreads();
+  TPX_PHASE(3);
 
   // ---- flatten (read-only root walk; every stored value is a final root)
   for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
@@ -429,8 +513,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     par[l] = c;
   }
   __syncthreads();
+  TPX_PHASE(4);
 
-  // ---- sizes (warp-aggregated by root), open flags, cross pairs
+  // ---- sizes (warp-aggregated by root), open flags, cross pairs; stage the
+  // tile hits for the reductions (region A is free now)
+  srec rq[kItemsPerThread];
 #pragma unroll
   for (int q = 0; q < kItemsPerThread; ++q) {
     const uint32_t j = threadIdx.x + q * kTileThreads;
@@ -439,6 +526,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     if (j < nt) {
       if ((__ffs(peers) - 1) == (int)lane) atomicAdd(&csize[r], (uint32_t)__popc(peers));
       if (hflag[j] & 1u) copen[r] = 1;
+      rq[q] = load_srec(S + t0 + j);
+      stile[j] = make_uint4((uint32_t)(srec_toa(rq[q]) - base), rq[q].xy, srec_tot(rq[q]), rq[q].idx);
     }
   }
   for (uint32_t h0 = 0; h0 < nf; h0 += kTileThreads) {
@@ -457,8 +546,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     }
   }
   __syncthreads();
+  TPX_PHASE(5);
 
-  // ---- compact roots (stage rank) and multi-hit roots (accumulator slot)
+  // ---- compact roots (stage rank) and member offsets of multi-hit components
   {
     uint32_t packed[kItemsPerThread];
     uint32_t my = 0;
@@ -466,132 +556,98 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
     for (int q = 0; q < kItemsPerThread; ++q) {
       const uint32_t j = threadIdx.x * kItemsPerThread + q;  // blocked for rank order
       uint32_t v = 0;
-      if (j < nt && par[j] == j) v = 1u | ((csize[j] >= 2 ? 1u : 0u) << 16);
+      if (j < nt && par[j] == j) {
+        const uint32_t sz = csize[j];
+        v = 1u | ((sz >= 2 ? sz : 0u) << 16);
+      }
       packed[q] = v;
       my += v;
     }
-    uint32_t x = my;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= (unsigned)o) x += y;
-    }
-    if (lane == 31) s_wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t t = lane < kTileThreads / 32 ? s_wsum[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, t, o);
-        if (lane >= (unsigned)o) t += y;
-      }
-      if (lane < kTileThreads / 32) s_wsum[lane] = t;
-    }
-    __syncthreads();
-    uint32_t ex = (warp ? s_wsum[warp - 1] : 0) + x - my;
-    const uint32_t total = s_wsum[kTileThreads / 32 - 1];
+    uint32_t total;
+    uint32_t ex = tile_block_scan(my, &total, s_wsum);
 #pragma unroll
     for (int q = 0; q < kItemsPerThread; ++q) {
       const uint32_t j = threadIdx.x * kItemsPerThread + q;
       if (packed[q]) {
         crank[j] = (uint16_t)(ex & 0xffffu);
-        if (packed[q] >> 16) {
-          const uint32_t s = ex >> 16;
-          cacc[j] = (uint16_t)s;
-          a_tot[s] = 0;
-          a_sx[s] = 0;
-          a_sy[s] = 0;
-          a_vxl[s] = 0;
-          a_vxh[s] = 0;
-          a_vyl[s] = 0;
-          a_vyh[s] = 0;
-          a_tmin[s] = 0xffffffffu;
-          a_tmax[s] = 0;
-          a_midx[s] = 0xffffffffu;
-        }
+        coff[j] = (uint16_t)(ex >> 16);
+        ccur[j] = 0;
+        if ((packed[q] >> 16) >= kBigComp) big[atomicAdd(&s_nbig, 1u)] = (uint16_t)j;
       }
       ex += packed[q];
     }
     if (threadIdx.x == 0) a.comp_count[blockIdx.x] = total & 0xffffu;
   }
   __syncthreads();
-
-  // ---- feature reductions of multi-hit components: lanes of a warp that
-  // share a root reduce with REDUX first, then one shared-memory atomic per
-  // field and group (64-bit sums are split into 16-bit halves so that every
-  // atomic is a native 32-bit one: no CAS loops).
-  srec rq[kItemsPerThread];
+  // member array: hits of every multi-hit component, contiguous per component
 #pragma unroll
   for (int q = 0; q < kItemsPerThread; ++q) {
     const uint32_t j = threadIdx.x + q * kTileThreads;
-    uint32_t key = 0xffffffffu;
     if (j < nt) {
-      rq[q] = load_srec(S + t0 + j);
       const uint32_t r = par[j];
-      if (csize[r] >= 2) key = cacc[r];
-    }
-    const unsigned peers = __match_any_sync(kFull, key);
-    uint32_t tot = 0, x = 0, y = 0, rel = 0, idx = 0;
-    if (key != 0xffffffffu) {
-      tot = srec_tot(rq[q]);
-      x = srec_x(rq[q]);
-      y = srec_y(rq[q]);
-      rel = (uint32_t)(srec_toa(rq[q]) - base);
-      idx = rq[q].idx;
-    }
-    const uint32_t vx = tot * x, vy = tot * y;  // < 2^31 (tot < 2^16, x, y < 2^15)
-    const uint32_t s_tot = __reduce_add_sync(peers, tot);
-    const uint32_t s_x = __reduce_add_sync(peers, x);
-    const uint32_t s_y = __reduce_add_sync(peers, y);
-    const uint32_t s_vxl = __reduce_add_sync(peers, vx & 0xffffu);
-    const uint32_t s_vxh = __reduce_add_sync(peers, vx >> 16);
-    const uint32_t s_vyl = __reduce_add_sync(peers, vy & 0xffffu);
-    const uint32_t s_vyh = __reduce_add_sync(peers, vy >> 16);
-    const uint32_t m_tmin = __reduce_min_sync(peers, rel);
-    const uint32_t m_tmax = __reduce_max_sync(peers, rel);
-    const uint32_t m_idx = __reduce_min_sync(peers, idx);
-    if (key != 0xffffffffu && (__ffs(peers) - 1) == (int)lane) {
-      atomicAdd(&a_tot[key], s_tot);
-      atomicAdd(&a_sx[key], s_x);
-      atomicAdd(&a_sy[key], s_y);
-      atomicAdd(&a_vxl[key], s_vxl);
-      atomicAdd(&a_vxh[key], s_vxh);
-      atomicAdd(&a_vyl[key], s_vyl);
-      atomicAdd(&a_vyh[key], s_vyh);
-      atomicMin(&a_tmin[key], m_tmin);
-      atomicMax(&a_tmax[key], m_tmax);
-      atomicMin(&a_midx[key], m_idx);
+      if (csize[r] >= 2) mem[coff[r] + atomicAdd(&ccur[r], 1u)] = (uint16_t)j;
     }
   }
   __syncthreads();
+  TPX_PHASE(6);
 
-  // ---- outputs: staged records, labels, bitmap, open lists
+  // ---- A7 reductions: small components by their root thread, large ones by
+  // a whole warp (shuffle reduction); records staged, labels kept in smem
+#pragma unroll
+  for (int q = 0; q < kItemsPerThread; ++q) {
+    const uint32_t j = threadIdx.x + q * kTileThreads;
+    if (j < nt && par[j] == j) {
+      const uint32_t sz = csize[j];
+      if (sz < kBigComp) {
+        feat_acc f;
+        f.init();
+        if (sz == 1) {
+          f.add(stile[j]);
+        } else {
+          const uint32_t o = coff[j];
+          for (uint32_t k = 0; k < sz; ++k) f.add(stile[mem[o + k]]);
+        }
+        mlabel[j] = f.midx;
+        stage_write(a.stage + t0 + crank[j], f.midx, sz, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
+                    f.sty);
+      }
+    }
+  }
+  for (;;) {
+    uint32_t bi = 0;
+    if (lane == 0) bi = atomicAdd(&s_bigq, 1u);
+    bi = __shfl_sync(kFull, bi, 0);
+    if (bi >= s_nbig) break;
+    const uint32_t r = big[bi], sz = csize[r], o = coff[r];
+    feat_acc f;
+    f.init();
+    for (uint32_t k = lane; k < sz; k += 32) f.add(stile[mem[o + k]]);
+    f.warp_reduce();
+    if (lane == 0) {
+      mlabel[r] = f.midx;
+      stage_write(a.stage + t0 + crank[r], f.midx, sz, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx, f.sty);
+    }
+  }
+  __syncthreads();
+  TPX_PHASE(7);
+
+  // ---- outputs: labels, bitmap, open lists
 #pragma unroll
   for (int q = 0; q < kItemsPerThread; ++q) {
     const uint32_t j = threadIdx.x + q * kTileThreads;
     const bool v = j < nt;
-    uint32_t r = 0;
-    bool is_root = false, open = false, multi = false;
+    uint32_t r = 0, label = 0;
+    bool is_root = false, open = false;
     if (v) {
       r = par[j];
       is_root = r == j;
       open = copen[r] != 0;
-      multi = csize[r] >= 2;
+      label = mlabel[r];
     }
-    const uint32_t label = !v ? 0u : (multi ? a_midx[cacc[r]] : rq[q].idx);
     const uint64_t pos = t0 + j;
-    if (is_root) {  // staged record for every component root
-      const uint64_t slot = t0 + crank[j];
-      if (multi) {
-        const uint32_t s = cacc[j];
-        stage_write(a.stage + slot, label, csize[j], base + a_tmin[s], base + a_tmax[s], a_tot[s], a_sx[s], a_sy[s],
-                    ((uint64_t)a_vxh[s] << 16) + a_vxl[s], ((uint64_t)a_vyh[s] << 16) + a_vyl[s]);
-      } else {
-        const uint64_t toa = srec_toa(rq[q]), tot = srec_tot(rq[q]), x = srec_x(rq[q]), y = srec_y(rq[q]);
-        stage_write(a.stage + slot, label, 1, toa, toa, tot, x, y, tot * x, tot * y);
-      }
+    if (is_root) {
       if (!open) set_label_bit(a.bitmap, label);
-      else a.slot_of[pos] = (uint32_t)slot;
+      else a.slot_of[pos] = (uint32_t)(t0 + crank[j]);
     }
     const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);
     if (is_root && open) a.open_comps[oc] = (uint32_t)pos;
@@ -609,6 +665,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_cc(tile_args a) {
       if (ovf) a.overflow[ov] = (uint32_t)pos;
     }
   }
+  TPX_PHASE(8);
 }
 
 }  // namespace tpx

@@ -280,6 +280,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.overflow = overflow;
   a.hdr = hdr;
   a.verify_stride = kWSortTile;
+  a.phase_cycles = c->profiling ? hdr->phase_cycles : nullptr;
   k_tile_cc<<<L.tiles, kTileThreads, kTileSmem, r.s>>>(a);
   TPX_LAUNCHED(c);
 
@@ -479,6 +480,9 @@ int tpx_cluster_run(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* l
   *n_clusters_out = k;
   c->stats.n_clusters = k;
   c->stats.cross_pairs = h.n_pairs;
+  c->stats.open_hits = h.n_open_hits;
+  c->stats.overflow_hits = h.n_overflow;
+  for (int i = 0; i < 16; ++i) c->stats.tile_phase_cycles[i] = h.phase_cycles[i];
   if (c->profiling) {
     c->stats.n_stages = 4;
     for (int i = 0; i < 4; ++i) {
