@@ -127,6 +127,20 @@ int tpx_cluster_run(tpx_cluster* ctx, const tpx_hit* hits, uint64_t n,
                     uint64_t capacity, uint64_t* n_clusters_out,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* tpx_cluster_run for a sharded rank: the first n_owned hits are this rank's
+ * own, the remaining n - n_owned are a halo borrowed from the next rank.
+ * Connectivity uses all n hits; features count only the owned hits, and
+ * records are produced only for clusters whose label (smallest input index)
+ * is < n_owned (the halo must be stored after the owned hits).  labels_out
+ * covers all n hits.  Same buffers, errors and synchronisation as
+ * tpx_cluster_run (which is run_partial with n_owned = n). */
+int tpx_cluster_run_partial(tpx_cluster* ctx, const tpx_hit* hits, uint64_t n,
+                            uint64_t n_owned, uint32_t* labels_out,
+                            tpx_cluster_features* features_out,
+                            uint64_t capacity, uint64_t* n_clusters_out,
+                            void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* Device workspace needed by tpx_cluster_run_host: device staging for the
  * hits, labels and `capacity` feature records plus tpx_cluster_run's own. */
 int tpx_cluster_host_workspace_bytes(const tpx_cluster* ctx, uint64_t n,
@@ -179,6 +193,98 @@ int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
 
 /* Static name of stage i (0 <= i < 16) as reported in stage_ms; "" if unused. */
 const char* tpx_cluster_stage_name(int i);
+
+/* ------------------------------------------------------------------------
+ * ToA-sharded multi-GPU building blocks (one process per GPU).
+ *
+ * Rank r owns the contiguous input-index block [o_r, o_r + n_r) of the
+ * t-ordered stream (§3.1 l.99-100).  Edges only join hits within
+ * dt_max in ToA (§2 (iii)(a) l.39), so rank r needs only rank r+1's hits with
+ * toa <= maxToA(r) + dt_max (the temporal-splitting border region, §3.2.3
+ * l.117-119), provided no edge can skip a rank (minToA(r+2) > maxToA(r) +
+ * dt_max, checked by the caller from the gathered ranges).  The collectives
+ * between these calls (all-gather of sizes/ranges/pairs/partials, halo
+ * send/recv) are issued by the caller on its process group (NCCL over
+ * NVLink); every compute step below is a device kernel.  All pointers are
+ * DEVICE pointers, all calls are stream-ordered and asynchronous unless
+ * stated, `count`-style outputs are device uint64 written by the call.
+ * ---------------------------------------------------------------------- */
+
+/* minmax[0] = min toa, minmax[1] = max toa of n hits (n = 0: ~0, 0). */
+int tpx_shard_toa_range(const tpx_hit* hits, uint64_t n, uint64_t* minmax,
+                        void* stream);
+
+int tpx_shard_select_workspace_bytes(uint64_t n, size_t* bytes);
+
+/* Halo for the previous rank: the hits with toa <= toa_limit, compacted in
+ * input order into halo_out, their positions (0-based, this rank's block)
+ * into idx_out; *count = how many.  Capacity of halo_out / idx_out: n. */
+int tpx_shard_select_halo(const tpx_hit* hits, uint64_t n, uint64_t toa_limit,
+                          tpx_hit* halo_out, uint32_t* idx_out,
+                          uint64_t* count, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* Local labels of [owned (n_owned) | halo (n - n_owned)] -> global input
+ * indices: L < n_owned -> own_offset + L, else next_offset + halo_idx[L - n_owned]. */
+int tpx_shard_translate_labels(uint32_t* labels, uint64_t n, uint64_t n_owned,
+                               uint64_t own_offset, const uint32_t* halo_idx,
+                               uint64_t next_offset, void* stream);
+
+/* features[i].label += offset for i < k (local -> global labels). */
+int tpx_shard_offset_labels(tpx_cluster_features* features, uint64_t k,
+                            uint64_t offset, void* stream);
+
+/* out[k] = labels[idx[k]], k < count (labels of the hits sent as halo). */
+int tpx_shard_gather_labels(const uint32_t* labels, const uint32_t* idx,
+                            uint64_t count, uint32_t* out, void* stream);
+
+/* Boundary pairs: (a[k], b[k]) for every k with a[k] != b[k], compacted into
+ * pairs_out (2 u32 per pair, capacity 2*count); *n_pairs = how many. */
+int tpx_shard_make_pairs(const uint32_t* a, const uint32_t* b, uint64_t count,
+                         uint32_t* pairs_out, uint64_t* n_pairs, void* stream);
+
+int tpx_shard_union_workspace_bytes(uint64_t n_pairs, size_t* bytes);
+
+/* Union pass over all ranks' pairs (n_pairs known on the host): map_keys =
+ * the distinct labels appearing in pairs, ascending; map_vals = the smallest
+ * label connected to each; *n_map = number of keys (capacity 2*n_pairs). */
+int tpx_shard_union_pairs(const uint32_t* pairs, uint64_t n_pairs,
+                          uint32_t* map_keys, uint32_t* map_vals,
+                          uint64_t* n_map, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* labels[i] <- map(labels[i]) for labels that are map keys. */
+int tpx_shard_relabel(uint32_t* labels, uint64_t n, const uint32_t* map_keys,
+                      const uint32_t* map_vals, const uint64_t* n_map,
+                      void* stream);
+
+int tpx_shard_split_workspace_bytes(uint64_t k, size_t* bytes);
+
+/* Split k label-sorted records: records whose label is a map key become
+ * partials keyed by their final label (partials_out, *n_partials, any order);
+ * the others are kept in order (kept_out, *n_kept).  Capacities: k each. */
+int tpx_shard_split_features(const tpx_cluster_features* features, uint64_t k,
+                             const uint32_t* map_keys, const uint32_t* map_vals,
+                             const uint64_t* n_map,
+                             tpx_cluster_features* kept_out, uint64_t* n_kept,
+                             tpx_cluster_features* partials_out,
+                             uint64_t* n_partials, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+int tpx_shard_fold_workspace_bytes(uint64_t n_partials, size_t* bytes);
+
+/* Owner fold: partials (all ranks') with label in [label_lo, label_hi) are
+ * combined per label (integer add / min / max: order independent, exact) and
+ * merged with the kept records into out (ascending label).  *n_out (HOST) =
+ * record count; synchronises the stream.  TPX_ERR_CAPACITY if it exceeds
+ * capacity. */
+int tpx_shard_fold_features(const tpx_cluster_features* kept, uint64_t n_kept,
+                            const tpx_cluster_features* partials,
+                            uint64_t n_partials, uint64_t label_lo,
+                            uint64_t label_hi, tpx_cluster_features* out,
+                            uint64_t capacity, uint64_t* n_out,
+                            void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 #ifdef __cplusplus
 }

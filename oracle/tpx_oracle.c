@@ -57,7 +57,7 @@ typedef struct pix_index {
   uint32_t* order;   /* hit ids, bucketed, (toa, id)-sorted       */
 } pix_index;
 
-static const ohit* g_sort_hits; /* qsort context (single-threaded oracle) */
+static _Thread_local const ohit* g_sort_hits; /* qsort context (one per calling thread) */
 static int cmp_toa_id(const void* a, const void* b) {
   uint32_t i = *(const uint32_t*)a, j = *(const uint32_t*)b;
   uint64_t ti = g_sort_hits[i].toa, tj = g_sort_hits[j].toa;

@@ -69,6 +69,26 @@ _centroids = _proto("tpx_cluster_centroids", _int, _vp, _u64, _vp, _vp)
 _last_stats = _proto("tpx_cluster_last_stats", _int, _vp, ctypes.POINTER(RunStats))
 _set_profiling = _proto("tpx_cluster_set_profiling", _int, _vp, _int)
 _stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
+_run_partial = _proto("tpx_cluster_run_partial", _int, _vp, _vp, _u64, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
+                      _vp, ctypes.c_size_t, _vp)
+_size_t_p = ctypes.POINTER(ctypes.c_size_t)
+# sharded building blocks (include/tpx_cluster.h, "ToA-sharded multi-GPU")
+_shard_toa_range = _proto("tpx_shard_toa_range", _int, _vp, _u64, _vp, _vp)
+_shard_select_ws = _proto("tpx_shard_select_workspace_bytes", _int, _u64, _size_t_p)
+_shard_select = _proto("tpx_shard_select_halo", _int, _vp, _u64, _u64, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp)
+_shard_translate = _proto("tpx_shard_translate_labels", _int, _vp, _u64, _u64, _u64, _vp, _u64, _vp)
+_shard_gather = _proto("tpx_shard_gather_labels", _int, _vp, _vp, _u64, _vp, _vp)
+_shard_offset = _proto("tpx_shard_offset_labels", _int, _vp, _u64, _u64, _vp)
+_shard_pairs = _proto("tpx_shard_make_pairs", _int, _vp, _vp, _u64, _vp, _vp, _vp)
+_shard_union_ws = _proto("tpx_shard_union_workspace_bytes", _int, _u64, _size_t_p)
+_shard_union = _proto("tpx_shard_union_pairs", _int, _vp, _u64, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp)
+_shard_relabel = _proto("tpx_shard_relabel", _int, _vp, _u64, _vp, _vp, _vp, _vp)
+_shard_split_ws = _proto("tpx_shard_split_workspace_bytes", _int, _u64, _size_t_p)
+_shard_split = _proto("tpx_shard_split_features", _int, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                      ctypes.c_size_t, _vp)
+_shard_fold_ws = _proto("tpx_shard_fold_workspace_bytes", _int, _u64, _size_t_p)
+_shard_fold = _proto("tpx_shard_fold_features", _int, _vp, _u64, _vp, _u64, _u64, _u64, _vp, _u64,
+                     ctypes.POINTER(_u64), _vp, ctypes.c_size_t, _vp)
 
 ABI_VERSION = _abi_version()
 
@@ -77,6 +97,17 @@ class TpxError(RuntimeError):
     def __init__(self, status: int, what: str = ""):
         self.status = status
         super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+def _check(rc: int, what: str):
+    if rc != TPX_OK:
+        raise TpxError(rc, what)
+
+
+def _size_query(fn, n: int) -> int:
+    b = ctypes.c_size_t(0)
+    _check(fn(int(n), ctypes.byref(b)), fn.__name__)
+    return b.value
 
 
 def status_string(status: int) -> str:
@@ -186,6 +217,21 @@ class Clusterer:
             raise TpxError(rc, "tpx_cluster_run")
         kk = min(k.value, capacity)
         return labels[:n], features[:kk], k.value
+
+    def run_partial(self, hits, n: int, n_owned: int, stream=None):
+        """``tpx_cluster_run_partial``: the first n_owned hits are owned, the rest
+        a borrowed halo (features and records only from owned hits)."""
+        torch = _torch()
+        dev = hits.device
+        labels = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        features = torch.empty((max(n_owned, 1), 64), dtype=torch.uint8, device=dev)
+        workspace = self._workspace(self.workspace_bytes(n), dev)
+        k = _u64(0)
+        rc = _run_partial(self._h, hits.data_ptr(), int(n), int(n_owned), labels.data_ptr(), features.data_ptr(),
+                          int(n_owned), ctypes.byref(k), workspace.data_ptr(), workspace.numel(),
+                          _stream_handle(stream))
+        _check(rc, "tpx_cluster_run_partial")
+        return labels[:n], features[: k.value], k.value
 
     def run_host(self, hits_host, labels_host, features_host, capacity: int | None = None, workspace=None,
                  stream=None, check: bool = True) -> int:

@@ -54,18 +54,19 @@ __global__ void k_labels(const srec* __restrict__ rec, const uint32_t* __restric
 }
 
 // A6: flag[j] = (labels[j] == j)  (j is the label of its cluster).
-__global__ void k_flags(const uint32_t* __restrict__ labels, uint64_t n, uint32_t* __restrict__ flags) {
+__global__ void k_flags(const uint32_t* __restrict__ labels, uint64_t n, uint64_t n_owned,
+                        uint32_t* __restrict__ flags) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x)
-    flags[j] = labels[j] == (uint32_t)j;
+    flags[j] = labels[j] == (uint32_t)j && j < n_owned;
 }
 
 // Feature records initialised at their ordinal (ascending label).
 __global__ void k_feat_init(const uint32_t* __restrict__ labels, const uint32_t* __restrict__ ord, uint64_t n,
-                            tpx_cluster_features* __restrict__ feats, uint64_t capacity) {
+                            uint64_t n_owned, tpx_cluster_features* __restrict__ feats, uint64_t capacity) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    if (labels[j] != (uint32_t)j) continue;
+    if (labels[j] != (uint32_t)j || !(j + 1 <= n_owned)) continue;
     uint32_t k = ord[j];
     if (k >= capacity) continue;
     tpx_cluster_features f;
@@ -81,10 +82,11 @@ __global__ void k_feat_init(const uint32_t* __restrict__ labels, const uint32_t*
 // A7: integer feature reductions (u64 atomics; order-independent, bit-exact).
 __global__ void k_feat_accum(const srec* __restrict__ rec, const uint32_t* __restrict__ root,
                              const uint32_t* __restrict__ minidx, const uint32_t* __restrict__ ord, uint64_t n,
-                             tpx_cluster_features* feats, uint64_t capacity) {
+                             uint64_t n_owned, tpx_cluster_features* feats, uint64_t capacity) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     srec r = load_srec(rec + i);
+    if (r.idx >= n_owned) continue;  // halo hit of a sharded run: no features
     uint32_t k = ord[minidx[root[i]]];
     if (k >= capacity) continue;
     tpx_cluster_features* f = feats + k;

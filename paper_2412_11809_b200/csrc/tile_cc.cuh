@@ -47,6 +47,7 @@ struct tile_args {
   uint64_t n;
   uint64_t dt;
   uint32_t width;
+  uint32_t n_owned;          // hits with input index >= n_owned carry no features (sharded halo)
   uint32_t bucket_shift;     // bucket = x >> bucket_shift  (< kBuckets buckets)
   uint32_t* labels;          // labels_out (input order)
   uint32_t* parent_g;        // global union-find over sorted positions (open hits only)
@@ -213,21 +214,27 @@ __device__ __forceinline__ uint32_t tile_block_scan(uint32_t v, uint32_t* total,
   return r;
 }
 
+// Feature accumulator.  Only hits with input index < n_owned contribute
+// features (sharded runs: halo hits connect clusters but belong to the next
+// rank); the label (smallest input index) is taken over all hits.
 struct feat_acc {
-  uint32_t tmin, tmax, midx;
+  uint32_t tmin, tmax, midx, cnt;
   uint64_t tot, sx, sy, stx, sty;
   __device__ __forceinline__ void init() {
     tmin = 0xffffffffu;
     tmax = 0;
     midx = 0xffffffffu;
+    cnt = 0;
     tot = sx = sy = stx = sty = 0;
   }
   // one staged hit: (toa - base, y<<16|x, tot, input index)
-  __device__ __forceinline__ void add(const uint4 h) {
+  __device__ __forceinline__ void add(const uint4 h, uint32_t n_owned) {
+    midx = min(midx, h.w);
+    if (h.w >= n_owned) return;
     const uint32_t x = h.y & 0xffffu, y = h.y >> 16, t = h.z;
+    cnt += 1;
     tmin = min(tmin, h.x);
     tmax = max(tmax, h.x);
-    midx = min(midx, h.w);
     tot += t;
     sx += x;
     sy += y;
@@ -240,6 +247,7 @@ struct feat_acc {
       tmin = min(tmin, __shfl_xor_sync(kFull, tmin, o));
       tmax = max(tmax, __shfl_xor_sync(kFull, tmax, o));
       midx = min(midx, __shfl_xor_sync(kFull, midx, o));
+      cnt += __shfl_xor_sync(kFull, cnt, o);
       tot += __shfl_xor_sync(kFull, tot, o);
       sx += __shfl_xor_sync(kFull, sx, o);
       sy += __shfl_xor_sync(kFull, sy, o);
@@ -392,10 +400,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
       const uint32_t ov = warp_append(v, &a.hdr->n_overflow);
       if (v) {
         const uint64_t pos = t0 + j;
-        const uint64_t toa = srec_toa(r), tot = srec_tot(r), x = srec_x(r), y = srec_y(r);
+        const bool own = r.idx < a.n_owned;
+        const uint64_t toa = srec_toa(r), tot = own ? srec_tot(r) : 0, x = own ? srec_x(r) : 0,
+                       y = own ? srec_y(r) : 0;
         a.parent_g[pos] = (uint32_t)pos;
         a.slot_of[pos] = (uint32_t)(t0 + j);
-        stage_write(a.stage + t0 + j, r.idx, 1, toa, toa, tot, x, y, tot * x, tot * y);
+        stage_write(a.stage + t0 + j, r.idx, own ? 1 : 0, own ? toa : ~0ull, own ? toa : 0, tot, x, y, tot * x,
+                    tot * y);
         a.open_hits[oh] = (uint32_t)pos;
         a.open_comps[oc] = (uint32_t)pos;
         a.overflow[ov] = (uint32_t)pos;
@@ -602,13 +613,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
         feat_acc f;
         f.init();
         if (sz == 1) {
-          f.add(stile[j]);
+          f.add(stile[j], a.n_owned);
         } else {
           const uint32_t o = coff[j];
-          for (uint32_t k = 0; k < sz; ++k) f.add(stile[mem[o + k]]);
+          for (uint32_t k = 0; k < sz; ++k) f.add(stile[mem[o + k]], a.n_owned);
         }
         mlabel[j] = f.midx;
-        stage_write(a.stage + t0 + crank[j], f.midx, sz, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
+        stage_write(a.stage + t0 + crank[j], f.midx, f.cnt, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
                     f.sty);
       }
     }
@@ -621,11 +632,12 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
     const uint32_t r = big[bi], sz = csize[r], o = coff[r];
     feat_acc f;
     f.init();
-    for (uint32_t k = lane; k < sz; k += 32) f.add(stile[mem[o + k]]);
+    for (uint32_t k = lane; k < sz; k += 32) f.add(stile[mem[o + k]], a.n_owned);
     f.warp_reduce();
     if (lane == 0) {
       mlabel[r] = f.midx;
-      stage_write(a.stage + t0 + crank[r], f.midx, sz, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx, f.sty);
+      stage_write(a.stage + t0 + crank[r], f.midx, f.cnt, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
+                  f.sty);
     }
   }
   __syncthreads();
@@ -646,7 +658,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
     }
     const uint64_t pos = t0 + j;
     if (is_root) {
-      if (!open) set_label_bit(a.bitmap, label);
+      if (!open && label < a.n_owned) set_label_bit(a.bitmap, label);
       else a.slot_of[pos] = (uint32_t)(t0 + crank[j]);
     }
     const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);

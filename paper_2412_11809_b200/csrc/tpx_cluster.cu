@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "finalize.cuh"
 #include "scan.cuh"
+#include "shard.cuh"
 #include "sort.cuh"
 #include "sort_window.cuh"
 #include "tile_cc.cuh"
@@ -195,6 +196,7 @@ static int radix_sort(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t 
 struct run_ptrs {
   const tpx_hit* hits;
   uint64_t n;
+  uint64_t n_owned;
   uint32_t* labels;
   tpx_cluster_features* feats;
   uint64_t capacity;
@@ -266,6 +268,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.n = r.n;
   a.dt = c->dt;
   a.width = c->width;
+  a.n_owned = (uint32_t)r.n_owned;
   a.bucket_shift = 0;
   while (((c->width - 1) >> a.bucket_shift) >= (uint32_t)kBuckets) ++a.bucket_shift;
   a.labels = r.labels;
@@ -292,7 +295,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   k_merge_open<<<kListGrid, kListThreads, 0, r.s>>>(open_comps, hdr, parent_g, slot_of, stage);
   TPX_LAUNCHED(c);
   k_open_labels<<<kListGrid, kListThreads, 0, r.s>>>(S, open_hits, open_comps, hdr, parent_g, slot_of, stage,
-                                                     r.labels, bitmap);
+                                                     r.labels, bitmap, (uint32_t)r.n_owned);
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[3], r.s);
@@ -334,15 +337,15 @@ static int cluster_global(tpx_cluster* c, const run_ptrs& r) {
   TPX_LAUNCHED(c);
   k_labels<<<grid_for(n, 256), 256, 0, r.s>>>(S, parent, minidx, n, r.labels);
   TPX_LAUNCHED(c);
-  k_flags<<<grid_for(n, 256), 256, 0, r.s>>>(r.labels, n, flags);
+  k_flags<<<grid_for(n, 256), 256, 0, r.s>>>(r.labels, n, r.n_owned, flags);
   TPX_LAUNCHED(c);
   if (c->profiling) cudaEventRecord(c->ev[3], r.s);
   int rc = exclusive_scan(c, flags, n, ord, partials, (uint32_t*)&hdr->n_clusters, r.s);
   if (rc) return rc;
   if (r.capacity) {
-    k_feat_init<<<grid_for(n, 256), 256, 0, r.s>>>(r.labels, ord, n, r.feats, r.capacity);
+    k_feat_init<<<grid_for(n, 256), 256, 0, r.s>>>(r.labels, ord, n, r.n_owned, r.feats, r.capacity);
     TPX_LAUNCHED(c);
-    k_feat_accum<<<grid_for(n, 256), 256, 0, r.s>>>(S, parent, minidx, ord, n, r.feats, r.capacity);
+    k_feat_accum<<<grid_for(n, 256), 256, 0, r.s>>>(S, parent, minidx, ord, n, r.n_owned, r.feats, r.capacity);
     TPX_LAUNCHED(c);
   }
   if (c->profiling) cudaEventRecord(c->ev[4], r.s);
@@ -419,9 +422,17 @@ int tpx_cluster_last_stats(const tpx_cluster* c, tpx_run_stats* out) {
 int tpx_cluster_run(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* labels_out,
                     tpx_cluster_features* features_out, uint64_t capacity, uint64_t* n_clusters_out, void* workspace,
                     size_t workspace_bytes, void* stream) {
+  return tpx_cluster_run_partial(c, hits, n, n, labels_out, features_out, capacity, n_clusters_out, workspace,
+                                 workspace_bytes, stream);
+}
+
+int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t n_owned, uint32_t* labels_out,
+                            tpx_cluster_features* features_out, uint64_t capacity, uint64_t* n_clusters_out,
+                            void* workspace, size_t workspace_bytes, void* stream) {
   if (!c || !n_clusters_out) return TPX_ERR_INVALID_ARG;
   *n_clusters_out = 0;
   if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
+  if (n_owned > n) return TPX_ERR_INVALID_ARG;
   memset(&c->stats, 0, sizeof(c->stats));
   c->stats.n_hits = n;
   if (n == 0) return TPX_OK;
@@ -435,6 +446,7 @@ int tpx_cluster_run(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* l
   if (ensure_cuda(c)) return TPX_ERR_CUDA;
   r.hits = hits;
   r.n = n;
+  r.n_owned = n_owned;
   r.labels = labels_out;
   r.feats = features_out;
   r.capacity = capacity;
@@ -538,6 +550,281 @@ int tpx_cluster_centroids(const tpx_cluster_features* features, uint64_t k, doub
   k_centroids<<<grid_for(k, 256), 256, 0, (cudaStream_t)stream>>>(features, k, cxy);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TPX_OK : TPX_ERR_CUDA;
+}
+
+}  // extern "C"
+
+// ============================================================ sharded path
+namespace {
+
+#define TPX_K(...)                                                                  \
+  do {                                                                              \
+    __VA_ARGS__;                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) {                                                        \
+      fprintf(stderr, "tpx_shard: launch failed: %s\n", cudaGetErrorString(e_));    \
+      return TPX_ERR_CUDA;                                                          \
+    }                                                                               \
+  } while (0)
+
+int scan_u32(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* partials, uint32_t* total, cudaStream_t s) {
+  const uint32_t tiles = n_tiles_of(n, kScanTile);
+  TPX_K(k_scan_reduce<<<tiles, kScanThreads, 0, s>>>(in, n, partials));
+  TPX_K(k_scan_partials<<<1, kScanThreads, 0, s>>>(partials, tiles, total));
+  TPX_K(k_scan_down<<<tiles, kScanThreads, 0, s>>>(in, n, partials, out));
+  return TPX_OK;
+}
+
+size_t scan_partials_bytes(uint64_t n) {
+  const uint32_t rt = n_tiles_of(n, kRadixTile);
+  uint32_t st = n_tiles_of((uint64_t)rt * kRadixBins, kScanTile);
+  st = st > n_tiles_of(n, kScanTile) ? st : n_tiles_of(n, kScanTile);
+  return (size_t)st * 4 + 64;
+}
+
+// Stable LSD radix sort of n u32 keys with u32 payload (4 passes, result in place).
+int sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, uint32_t* tk, uint32_t* tv, uint32_t* hist,
+             uint32_t* partials, cudaStream_t s) {
+  const uint32_t tiles = n_tiles_of(n, kRadixTile);
+  uint32_t *k0 = keys, *k1 = tk, *v0 = vals, *v1 = tv;
+  for (int p = 0; p < 4; ++p) {
+    TPX_K(k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, 8 * p, hist, tiles));
+    int rc = scan_u32(hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s);
+    if (rc) return rc;
+    TPX_K(k_radix_scatter<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, 8 * p, hist, tiles,
+                                                                        k1, v1));
+    uint32_t* t = k0;
+    k0 = k1;
+    k1 = t;
+    t = v0;
+    v0 = v1;
+    v1 = t;
+  }
+  return TPX_OK;  // 4 swaps: result is back in keys / vals
+}
+
+size_t sort_u32_ws(uint64_t n) {
+  return align256(n * 4) * 2 + align256((size_t)n_tiles_of(n, kRadixTile) * kRadixBins * 4) +
+         align256(scan_partials_bytes(n));
+}
+
+}  // namespace
+
+extern "C" {
+
+int tpx_shard_toa_range(const tpx_hit* hits, uint64_t n, uint64_t* minmax, void* stream) {
+  if (!minmax || (n && !hits)) return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  TPX_K(k_range_init<<<1, 1, 0, s>>>((unsigned long long*)minmax));
+  if (n) TPX_K(k_toa_range<<<grid_for(n, 256), 256, 0, s>>>(hits, n, (unsigned long long*)minmax));
+  return TPX_OK;
+}
+
+int tpx_shard_select_workspace_bytes(uint64_t n, size_t* bytes) {
+  if (!bytes) return TPX_ERR_INVALID_ARG;
+  *bytes = align256(n * 4) * 2 + align256(scan_partials_bytes(n)) + 256;
+  return TPX_OK;
+}
+
+int tpx_shard_select_halo(const tpx_hit* hits, uint64_t n, uint64_t toa_limit, tpx_hit* halo_out,
+                          uint32_t* idx_out, uint64_t* count, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  size_t need = 0;
+  tpx_shard_select_workspace_bytes(n, &need);
+  if (!count || workspace_bytes < need || (n && (!hits || !halo_out || !idx_out || !workspace)))
+    return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(count, 0, 8, s) != cudaSuccess) return TPX_ERR_CUDA;
+  if (n == 0) return TPX_OK;
+  char* ws = (char*)workspace;
+  uint32_t* flags = (uint32_t*)ws;
+  uint32_t* ord = (uint32_t*)(ws + align256(n * 4));
+  uint32_t* partials = (uint32_t*)(ws + 2 * align256(n * 4));
+  TPX_K(k_halo_flags<<<grid_for(n, 256), 256, 0, s>>>(hits, n, toa_limit, flags));
+  int rc = scan_u32(flags, n, ord, partials, (uint32_t*)count, s);
+  if (rc) return rc;
+  TPX_K(k_halo_scatter<<<grid_for(n, 256), 256, 0, s>>>(hits, n, flags, ord, halo_out, idx_out));
+  return TPX_OK;
+}
+
+int tpx_shard_translate_labels(uint32_t* labels, uint64_t n, uint64_t n_owned, uint64_t own_offset,
+                               const uint32_t* halo_idx, uint64_t next_offset, void* stream) {
+  if (n == 0) return TPX_OK;
+  if (!labels || n_owned > n || (n > n_owned && !halo_idx)) return TPX_ERR_INVALID_ARG;
+  TPX_K(k_translate<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(labels, n, n_owned, own_offset, halo_idx,
+                                                                         next_offset));
+  return TPX_OK;
+}
+
+int tpx_shard_offset_labels(tpx_cluster_features* features, uint64_t k, uint64_t offset, void* stream) {
+  if (k == 0) return TPX_OK;
+  if (!features || offset >= 0xffffffffull) return TPX_ERR_INVALID_ARG;
+  TPX_K(k_offset_labels<<<grid_for(k, 256), 256, 0, (cudaStream_t)stream>>>(features, k, (uint32_t)offset));
+  return TPX_OK;
+}
+
+int tpx_shard_gather_labels(const uint32_t* labels, const uint32_t* idx, uint64_t count, uint32_t* out,
+                            void* stream) {
+  if (count == 0) return TPX_OK;
+  if (!labels || !idx || !out) return TPX_ERR_INVALID_ARG;
+  TPX_K(k_gather_u32<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(labels, idx, count, out));
+  return TPX_OK;
+}
+
+int tpx_shard_make_pairs(const uint32_t* a, const uint32_t* b, uint64_t count, uint32_t* pairs_out,
+                         uint64_t* n_pairs, void* stream) {
+  if (!n_pairs || (count && (!a || !b || !pairs_out))) return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(n_pairs, 0, 8, s) != cudaSuccess) return TPX_ERR_CUDA;
+  if (count)
+    TPX_K(k_make_pairs<<<grid_for(count, 256), 256, 0, s>>>(a, b, count, (uint2*)pairs_out,
+                                                            (unsigned long long*)n_pairs));
+  return TPX_OK;
+}
+
+int tpx_shard_union_workspace_bytes(uint64_t n_pairs, size_t* bytes) {
+  if (!bytes) return TPX_ERR_INVALID_ARG;
+  const uint64_t m = 2 * n_pairs;
+  *bytes = align256(m * 4) * 6 + sort_u32_ws(m) + 512;
+  return TPX_OK;
+}
+
+int tpx_shard_union_pairs(const uint32_t* pairs, uint64_t n_pairs, uint32_t* map_keys, uint32_t* map_vals,
+                          uint64_t* n_map, void* workspace, size_t workspace_bytes, void* stream) {
+  size_t need = 0;
+  tpx_shard_union_workspace_bytes(n_pairs, &need);
+  if (!n_map || workspace_bytes < need || (n_pairs && (!pairs || !map_keys || !map_vals || !workspace)))
+    return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(n_map, 0, 8, s) != cudaSuccess) return TPX_ERR_CUDA;
+  if (n_pairs == 0) return TPX_OK;
+  const uint64_t m = 2 * n_pairs;
+  char* ws = (char*)workspace;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* p = ws + off;
+    off += align256(b);
+    return p;
+  };
+  uint32_t* keys = (uint32_t*)take(m * 4);
+  uint32_t* vals = (uint32_t*)take(m * 4);
+  uint32_t* flags = (uint32_t*)take(m * 4);
+  uint32_t* ord = (uint32_t*)take(m * 4);
+  uint32_t* parent = (uint32_t*)take(m * 4);
+  uint32_t* tmp = (uint32_t*)take(m * 4);
+  uint32_t* tk = (uint32_t*)take(m * 4);
+  uint32_t* tv = (uint32_t*)take(m * 4);
+  uint32_t* hist = (uint32_t*)take((size_t)n_tiles_of(m, kRadixTile) * kRadixBins * 4);
+  uint32_t* partials = (uint32_t*)take(scan_partials_bytes(m));
+  (void)tmp;
+  if (cudaMemcpyAsync(keys, pairs, m * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return TPX_ERR_CUDA;
+  int rc = sort_u32(keys, vals, m, tk, tv, hist, partials, s);
+  if (rc) return rc;
+  TPX_K(k_unique_flags<<<grid_for(m, 256), 256, 0, s>>>(keys, m, flags));
+  rc = scan_u32(flags, m, ord, partials, (uint32_t*)n_map, s);
+  if (rc) return rc;
+  TPX_K(k_unique_scatter<<<grid_for(m, 256), 256, 0, s>>>(keys, m, flags, ord, map_keys, parent));
+  TPX_K(k_pair_union<<<grid_for(n_pairs, 256), 256, 0, s>>>((const uint2*)pairs, n_pairs, map_keys,
+                                                            (const uint32_t*)n_map, parent));
+  TPX_K(k_pair_finals<<<grid_for(m, 256), 256, 0, s>>>(map_keys, (const uint32_t*)n_map, parent, map_vals));
+  return TPX_OK;
+}
+
+int tpx_shard_relabel(uint32_t* labels, uint64_t n, const uint32_t* map_keys, const uint32_t* map_vals,
+                      const uint64_t* n_map, void* stream) {
+  if (n == 0) return TPX_OK;
+  if (!labels || !map_keys || !map_vals || !n_map) return TPX_ERR_INVALID_ARG;
+  TPX_K(k_relabel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(labels, n, map_keys, map_vals,
+                                                                       (const unsigned long long*)n_map));
+  return TPX_OK;
+}
+
+int tpx_shard_split_workspace_bytes(uint64_t k, size_t* bytes) {
+  if (!bytes) return TPX_ERR_INVALID_ARG;
+  *bytes = align256(k * 4) * 2 + align256(scan_partials_bytes(k)) + 256;
+  return TPX_OK;
+}
+
+int tpx_shard_split_features(const tpx_cluster_features* feats, uint64_t k, const uint32_t* map_keys,
+                             const uint32_t* map_vals, const uint64_t* n_map, tpx_cluster_features* kept_out,
+                             uint64_t* n_kept, tpx_cluster_features* partials_out, uint64_t* n_partials,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  size_t need = 0;
+  tpx_shard_split_workspace_bytes(k, &need);
+  if (!n_kept || !n_partials || workspace_bytes < need ||
+      (k && (!feats || !map_keys || !map_vals || !n_map || !kept_out || !partials_out || !workspace)))
+    return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(n_kept, 0, 8, s) != cudaSuccess || cudaMemsetAsync(n_partials, 0, 8, s) != cudaSuccess)
+    return TPX_ERR_CUDA;
+  if (k == 0) return TPX_OK;
+  char* ws = (char*)workspace;
+  uint32_t* keep = (uint32_t*)ws;
+  uint32_t* ord = (uint32_t*)(ws + align256(k * 4));
+  uint32_t* partials = (uint32_t*)(ws + 2 * align256(k * 4));
+  TPX_K(k_split_flags<<<grid_for(k, 256), 256, 0, s>>>(feats, k, map_keys, map_vals, (const unsigned long long*)n_map,
+                                                       keep, partials_out, (unsigned long long*)n_partials));
+  int rc = scan_u32(keep, k, ord, partials, (uint32_t*)n_kept, s);
+  if (rc) return rc;
+  TPX_K(k_compact_records<<<grid_for(k, 256), 256, 0, s>>>(feats, k, keep, ord, kept_out));
+  return TPX_OK;
+}
+
+int tpx_shard_fold_workspace_bytes(uint64_t n_partials, size_t* bytes) {
+  if (!bytes) return TPX_ERR_INVALID_ARG;
+  const uint64_t q = n_partials ? n_partials : 1;
+  *bytes = align256(q * 4) * 4 + align256(q * 64) + sort_u32_ws(q) + 512;
+  return TPX_OK;
+}
+
+int tpx_shard_fold_features(const tpx_cluster_features* kept, uint64_t n_kept, const tpx_cluster_features* partials,
+                            uint64_t n_partials, uint64_t label_lo, uint64_t label_hi, tpx_cluster_features* out,
+                            uint64_t capacity, uint64_t* n_out, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  size_t need = 0;
+  tpx_shard_fold_workspace_bytes(n_partials, &need);
+  if (!n_out || workspace_bytes < need || !workspace || (n_kept && !kept) || (n_partials && !partials) ||
+      (capacity && !out))
+    return TPX_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t q = n_partials ? n_partials : 1;
+  char* ws = (char*)workspace;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* p = ws + off;
+    off += align256(b);
+    return p;
+  };
+  uint32_t* keys = (uint32_t*)take(q * 4);
+  uint32_t* vals = (uint32_t*)take(q * 4);
+  uint32_t* head = (uint32_t*)take(q * 4);
+  uint32_t* ord = (uint32_t*)take(q * 4);
+  tpx_cluster_features* merged = (tpx_cluster_features*)take(q * 64);
+  uint32_t* tk = (uint32_t*)take(q * 4);
+  uint32_t* tv = (uint32_t*)take(q * 4);
+  uint32_t* hist = (uint32_t*)take((size_t)n_tiles_of(q, kRadixTile) * kRadixBins * 4);
+  uint32_t* sp = (uint32_t*)take(scan_partials_bytes(q));
+  unsigned long long* cnt = (unsigned long long*)take(16);  // [0] in-block partials, [1] merged count (u32 low)
+  if (cudaMemsetAsync(cnt, 0, 16, s) != cudaSuccess || cudaMemsetAsync(keys, 0xff, q * 4, s) != cudaSuccess ||
+      cudaMemsetAsync(head, 0, q * 4, s) != cudaSuccess)
+    return TPX_ERR_CUDA;
+  if (n_partials) {
+    TPX_K(k_fold_keys<<<grid_for(n_partials, 256), 256, 0, s>>>(partials, n_partials, label_lo, label_hi, keys, vals,
+                                                                cnt));
+    int rc = sort_u32(keys, vals, q, tk, tv, hist, sp, s);
+    if (rc) return rc;
+    TPX_K(k_run_heads<<<grid_for(q, 256), 256, 0, s>>>(keys, cnt, head));
+    rc = scan_u32(head, q, ord, sp, (uint32_t*)(cnt + 1), s);
+    if (rc) return rc;
+    TPX_K(k_fold_runs<<<grid_for(q, 256), 256, 0, s>>>(partials, keys, vals, cnt, head, ord, merged));
+  }
+  TPX_K(k_merge_records<<<grid_for(n_kept + q, 256), 256, 0, s>>>(kept, n_kept, merged, (const uint32_t*)(cnt + 1),
+                                                                  out, capacity));
+  unsigned long long h[2];
+  if (cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return TPX_ERR_CUDA;
+  *n_out = n_kept + (uint32_t)h[1];
+  return *n_out > capacity ? TPX_ERR_CAPACITY : TPX_OK;
 }
 
 }  // extern "C"
