@@ -64,7 +64,7 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 }
 
 template <int IT>
-__global__ void __launch_bounds__(kWSortThreads, 1) k_window_sort(const tpx_hit* __restrict__ hits, uint64_t n,
+__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit* __restrict__ hits, uint64_t n,
                                                                    uint32_t width, uint32_t height,
                                                                    srec* __restrict__ out, dev_hdr* hdr) {
   using C = wsort_cfg<IT>;
@@ -107,20 +107,24 @@ __global__ void __launch_bounds__(kWSortThreads, 1) k_window_sort(const tpx_hit*
   const int bits = range ? 64 - __clzll(range) : 0;
   const int passes = (bits + 7) >> 3;
   uint32_t key[IT];
-  uint16_t val[IT];
+  uint32_t vl[IT];  // low 16 bits: window position (payload); high 16: rank within the warp
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
     key[r] = (uint32_t)(toa[r] - base);
-    val[r] = (uint16_t)p;
+    vl[r] = p;
   }
 
   // ---- stable LSD radix passes, 8 bits each, ranks via warp-private counters
+  // cnt is warp-major (cnt[w * 256 + d]): lanes of a warp touch banks d % 32,
+  // so counter traffic is (nearly) conflict-free; equal digits are grouped by
+  // __match_any_sync and only the group leader writes.
+  __shared__ uint32_t dsum[kWSortThreads / 32];
   for (int pass = 0; pass < passes || pass == 0; ++pass) {
     const int shift = pass * 8;
     for (int i = threadIdx.x; i < 256 * kWSortWarps; i += kWSortThreads) cnt[i] = 0;
     __syncthreads();
-    uint16_t lr[IT];
+    uint32_t* wc = cnt + warp * 256;
 #pragma unroll
     for (int r = 0; r < IT; ++r) {
       const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
@@ -128,48 +132,37 @@ __global__ void __launch_bounds__(kWSortThreads, 1) k_window_sort(const tpx_hit*
       const unsigned d = valid ? (key[r] >> shift) & 0xffu : 256u;
       const unsigned peers = __match_any_sync(kFull, d);
       uint32_t b = 0;
-      if (valid) b = cnt[d * kWSortWarps + warp];
-      lr[r] = (uint16_t)(b + __popc(peers & lanemask_lt()));
+      if (valid) b = wc[d];
+      vl[r] = (vl[r] & 0xffffu) | ((b + __popc(peers & lanemask_lt())) << 16);
       __syncwarp();
-      if (valid && (__ffs(peers) - 1) == (int)lane) cnt[d * kWSortWarps + warp] = b + __popc(peers);
+      if (valid && (__ffs(peers) - 1) == (int)lane) wc[d] = b + __popc(peers);
       __syncwarp();
     }
     __syncthreads();
-    // exclusive scan over cnt in (digit, warp) order: 8 consecutive entries per thread
+    // offsets in (digit, warp) order: thread d < 256 owns digit d
     {
-      constexpr int PT = 256 * kWSortWarps / kWSortThreads;  // 8
-      uint32_t loc[PT];
-      uint32_t s = 0;
+      uint32_t tot = 0;
+      if (threadIdx.x < 256) {
 #pragma unroll
-      for (int i = 0; i < PT; ++i) {
-        loc[i] = cnt[threadIdx.x * PT + i];
-        s += loc[i];
+        for (int w = 0; w < kWSortWarps; ++w) tot += cnt[w * 256 + threadIdx.x];
       }
-      // block exclusive scan of s (512 threads)
-      __shared__ uint32_t wsum[kWSortWarps];
-      uint32_t x = s;
+      uint32_t x = tot;  // inclusive scan of digit totals over threads 0..255 (warps 0..7)
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(kFull, x, o);
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
         if (lane >= (unsigned)o) x += y;
       }
-      if (lane == 31) wsum[warp] = x;
+      if (lane == 31) dsum[warp] = x;
       __syncthreads();
-      if (warp == 0) {
-        uint32_t t = lane < kWSortWarps ? wsum[lane] : 0;
+      if (threadIdx.x < 256) {
+        uint32_t basev = x - tot;
+        for (unsigned w2 = 0; w2 < warp; ++w2) basev += dsum[w2];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          uint32_t y = __shfl_up_sync(kFull, t, o);
-          if (lane >= (unsigned)o) t += y;
+        for (int w = 0; w < kWSortWarps; ++w) {
+          const uint32_t c = cnt[w * 256 + threadIdx.x];
+          cnt[w * 256 + threadIdx.x] = basev;
+          basev += c;
         }
-        if (lane < kWSortWarps) wsum[lane] = t;
-      }
-      __syncthreads();
-      uint32_t ex = (warp ? wsum[warp - 1] : 0) + x - s;
-#pragma unroll
-      for (int i = 0; i < PT; ++i) {
-        cnt[threadIdx.x * PT + i] = ex;
-        ex += loc[i];
       }
     }
     __syncthreads();
@@ -178,9 +171,9 @@ __global__ void __launch_bounds__(kWSortThreads, 1) k_window_sort(const tpx_hit*
       const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
       if (p < m) {
         const unsigned d = (key[r] >> shift) & 0xffu;
-        const uint32_t q = cnt[d * kWSortWarps + warp] + lr[r];
+        const uint32_t q = wc[d] + (vl[r] >> 16);
         skey[q] = key[r];
-        sval[q] = val[r];
+        sval[q] = (uint16_t)vl[r];
       }
     }
     __syncthreads();
@@ -190,7 +183,7 @@ __global__ void __launch_bounds__(kWSortThreads, 1) k_window_sort(const tpx_hit*
         const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
         if (p < m) {
           key[r] = skey[p];
-          val[r] = sval[p];
+          vl[r] = sval[p];
         }
       }
       __syncthreads();
