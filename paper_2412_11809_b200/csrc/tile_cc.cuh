@@ -32,9 +32,10 @@ namespace tpx {
 
 constexpr int kTileThreads = 256;
 constexpr int kTile = 1024;                    // tile hits per CTA
-constexpr int kHaloCap = 1024;                 // staged halo hits per side
+constexpr int kHaloCap = 1024;                 // staged forward-halo hits
+constexpr int kBackCap = 512;                  // staged back-halo hits (openness only)
 constexpr int kFwdMax = kTile + kHaloCap;      // tile + forward halo (local index l)
-constexpr int kBuckets = 2048;                 // column buckets (x >> shift)
+constexpr int kBuckets = 1024;                 // column buckets (x >> shift)
 constexpr int kBucketCap = 512;                // longer buckets: the tile takes the global path
 constexpr int kStageItems = kFwdMax / kTileThreads;        // 8
 constexpr int kItemsPerThread = kTile / kTileThreads;      // 4
@@ -168,7 +169,7 @@ struct tile_smem_layout {
   static constexpr size_t big = mem + (size_t)kTile * 2;                // u16   [kTile]
   static_assert(big + (size_t)kTile * 2 <= region_a, "reduction arrays alias region A");
   static constexpr size_t hb = region_a;                                // uint2 [kHaloCap] (later: mlabel u32)
-  static constexpr size_t bs = hb + (size_t)kHaloCap * 8;               // u32   [kBuckets + 4]
+  static constexpr size_t bs = hb + (size_t)kBackCap * 8;               // u32   [kBuckets + 4]
   static constexpr size_t par = bs + ((size_t)kBuckets + 4) * 4;        // u32   [kFwdMax]
   static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile]
   static constexpr size_t crank = csize + (size_t)kTile * 4;            // u16   [kTile]
@@ -183,7 +184,7 @@ struct tile_smem_layout {
   static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
   static constexpr size_t total = hflag + kTile;
 };
-static_assert((size_t)kTile * 4 <= (size_t)kHaloCap * 8, "mlabel aliases the back halo");
+static_assert((size_t)kTile * 4 <= (size_t)kBackCap * 8, "mlabel aliases the back halo");
 constexpr size_t kTileSmem = tile_smem_layout::total;
 constexpr uint32_t kBigComp = 24;  // components this large are reduced by a whole warp
 
@@ -257,7 +258,7 @@ struct feat_acc {
   }
 };
 
-__global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
+__global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
   using SL = tile_smem_layout;
   extern __shared__ __align__(16) unsigned char sm[];
   uint2* csort = reinterpret_cast<uint2*>(sm + SL::csort);      // (toa - base, y<<16|x), bucket-sorted
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile_cc(tile_args a) {
   // back halo, warp 1 the forward halo), sort verification
   if (warp == 0) {
     const uint64_t toa_first = srec_key_toa(S, t0);
-    const uint64_t blim = t0 > (uint64_t)kHaloCap ? t0 - kHaloCap : 0;
+    const uint64_t blim = t0 > (uint64_t)kBackCap ? t0 - kBackCap : 0;
     // back halo: first position with toa + dt >= toa_first
     const uint64_t b0 = warp_lower_bound(blim, t0, [&](uint64_t p) { return srec_key_toa(S, p) + dt >= toa_first; });
     if (lane == 0) {
