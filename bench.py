@@ -208,24 +208,37 @@ def run_ours(args):
     value = n / (ms * 1e-3) / 1e6  # Mhit/s
     clocks = clk.summary()
 
-    # ---- end to end through the C ABI with HOST buffers (pinned), H2D/D2H timed
+    # ---- end to end with HOST buffers (pinned): the tpx_pipeline_* API overlaps
+    # the H2D / D2H of one buffer with the kernels of the others (depth 3, the
+    # paper's stream overlap); every step copies its 3.2 GB of
+    # hits in and its labels + records out inside the timed region
     cap_host = max(n // 4, 1)
-    lab_host = torch.empty(n, dtype=torch.int32).pin_memory()
-    feat_host = torch.empty((cap_host, 64), dtype=torch.uint8).pin_memory()
-    del wsbuf
+    depth = 3
+    lab_host = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(depth)]
+    feat_host = [torch.empty((cap_host, 64), dtype=torch.uint8).pin_memory() for _ in range(depth)]
+    del wsbuf, labels, feats
     torch.cuda.empty_cache()
-    hws = torch.empty(c.host_workspace_bytes(n, cap_host), dtype=torch.uint8, device=dev)
-    kk = c.run_host(h_host, lab_host, feat_host, capacity=cap_host, workspace=hws, stream=stream)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(1, min(args.steps, 5))
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        kk = c.run_host(h_host, lab_host, feat_host, capacity=cap_host, workspace=hws, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    del hws
+    pipe = tpx.Pipeline(dt, max_hits=n, capacity=cap_host, depth=depth)
+    e2e_steps = max(2, min(args.steps, 6))
+
+    def run_pipe(nsteps):
+        tickets, ks = [], []
+        for i in range(nsteps):
+            if len(tickets) >= depth:
+                ks.append(pipe.wait(tickets.pop(0)))
+            tickets.append(pipe.submit(h_host, lab_host[i % depth], feat_host[i % depth], capacity=cap_host))
+        while tickets:
+            ks.append(pipe.wait(tickets.pop(0)))
+        return ks
+
+    run_pipe(depth)  # warm-up
+    pipe.mark(0)
+    ks = run_pipe(e2e_steps)
+    pipe.mark(1)
+    e2e_ms = pipe.elapsed_ms() / e2e_steps
+    kk = ks[-1]
+    pipe.close()
+    del pipe
 
     # ---- roofline of the dominant kernel (B_alg = 16 + 4 + 64/s_bar per hit)
     s_bar = n / max(k, 1)
@@ -265,7 +278,9 @@ def run_ours(args):
                    "l2": "inputs (16 B x n = %.1f GB) exceed L2 (126 MB); no flush" % (n * 16 / 1e9),
                    "parallelism": f"{ws} GPU"},
         "e2e": {"value": round(n / (e2e_ms * 1e-3) / 1e6, 2), "unit": "Mhit/s", "h2d_bytes_per_step": n * 16,
-                "d2h_bytes_per_step": n * 4 + min(kk, cap_host) * 64, "ms_per_step": round(e2e_ms, 3)},
+                "d2h_bytes_per_step": n * 4 + min(kk, cap_host) * 64, "ms_per_step": round(e2e_ms, 3),
+                "api": "tpx_pipeline_submit/wait (depth 3: copies of one buffer overlap the kernels of the others)",
+                "steps": e2e_steps},
         "gpu_launches": launches,
         "roofline": roof,
         "hbm_alg_gbs_whole_path": round(whole_path_gbs, 2),

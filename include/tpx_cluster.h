@@ -195,6 +195,56 @@ int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
 const char* tpx_cluster_stage_name(int i);
 
 /* ------------------------------------------------------------------------
+ * Host-buffer pipeline (copy/compute overlap across buffers).
+ *
+ * The paper's GPU driver copies a filled host buffer to the device, clusters
+ * it and copies the result back, with buffers cycling "in use" / "reusable"
+ * (Alg. "High-level GPU clustering") and copies hidden
+ * behind compute with CUDA streams (l.310).  A pipeline has `depth` slots,
+ * each with its own context, stream and slice of one caller-provided DEVICE
+ * workspace; one native worker thread per slot runs tpx_cluster_run_host on
+ * the buffers submitted to it (round robin), so H2D / D2H of one buffer
+ * overlap the kernels of another.  Every buffer is an independent closed
+ * stream (results identical to tpx_cluster_run_host).  Host buffers are
+ * owned by the caller and must stay valid (pinned recommended) until
+ * tpx_pipeline_wait returns for their ticket.
+ * ---------------------------------------------------------------------- */
+typedef struct tpx_pipeline tpx_pipeline;
+
+/* Device workspace for a pipeline of `depth` (1..16) slots, each able to hold
+ * max_hits hits and `capacity` feature records. */
+int tpx_pipeline_workspace_bytes(const tpx_cluster* proto, uint64_t max_hits,
+                                 uint64_t capacity, int depth, size_t* bytes);
+
+/* Create a pipeline on the current device (contexts as tpx_cluster_create).
+ * workspace: DEVICE, 256-B aligned, >= tpx_pipeline_workspace_bytes. */
+int tpx_pipeline_create(uint64_t dt_max_ticks, int variant, uint32_t width,
+                        uint32_t height, uint64_t max_hits, uint64_t capacity,
+                        int depth, void* workspace, size_t workspace_bytes,
+                        tpx_pipeline** out);
+
+/* Queue one HOST buffer (n <= max_hits, capacity <= the pipeline's);
+ * *ticket identifies it for tpx_pipeline_wait.  Non-blocking. */
+int tpx_pipeline_submit(tpx_pipeline* p, const tpx_hit* hits_host, uint64_t n,
+                        uint32_t* labels_host,
+                        tpx_cluster_features* features_host,
+                        uint64_t capacity, uint64_t* ticket);
+
+/* Block until buffer `ticket` is done; returns its tpx_cluster_run_host
+ * status and cluster count (HOST). Each ticket can be waited on once. */
+int tpx_pipeline_wait(tpx_pipeline* p, uint64_t ticket,
+                      uint64_t* n_clusters_out);
+
+/* Device timing across the slot streams: mark(0) records a start event on
+ * every slot stream, mark(1) a stop event; elapsed_ms = latest stop minus
+ * earliest start (CUDA events; synchronises on the stop events). */
+int tpx_pipeline_mark(tpx_pipeline* p, int which);
+int tpx_pipeline_elapsed_ms(tpx_pipeline* p, float* ms);
+
+/* Stop the workers (after finishing queued buffers) and free the slots. */
+void tpx_pipeline_destroy(tpx_pipeline* p);
+
+/* ------------------------------------------------------------------------
  * ToA-sharded multi-GPU building blocks (one process per GPU).
  *
  * Rank r owns the contiguous input-index block [o_r, o_r + n_r) of the

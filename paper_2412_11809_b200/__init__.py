@@ -72,6 +72,15 @@ _stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
 _run_partial = _proto("tpx_cluster_run_partial", _int, _vp, _vp, _u64, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
                       _vp, ctypes.c_size_t, _vp)
 _size_t_p = ctypes.POINTER(ctypes.c_size_t)
+# host-buffer pipeline (include/tpx_cluster.h, "Host-buffer pipeline")
+_pipe_ws = _proto("tpx_pipeline_workspace_bytes", _int, _vp, _u64, _u64, _int, _size_t_p)
+_pipe_create = _proto("tpx_pipeline_create", _int, _u64, _int, _u32, _u32, _u64, _u64, _int, _vp, ctypes.c_size_t,
+                      ctypes.POINTER(_vp))
+_pipe_submit = _proto("tpx_pipeline_submit", _int, _vp, _vp, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64))
+_pipe_wait = _proto("tpx_pipeline_wait", _int, _vp, _u64, ctypes.POINTER(_u64))
+_pipe_mark = _proto("tpx_pipeline_mark", _int, _vp, _int)
+_pipe_elapsed = _proto("tpx_pipeline_elapsed_ms", _int, _vp, ctypes.POINTER(ctypes.c_float))
+_pipe_destroy = _proto("tpx_pipeline_destroy", None, _vp)
 # sharded building blocks (include/tpx_cluster.h, "ToA-sharded multi-GPU")
 _shard_toa_range = _proto("tpx_shard_toa_range", _int, _vp, _u64, _vp, _vp)
 _shard_select_ws = _proto("tpx_shard_select_workspace_bytes", _int, _u64, _size_t_p)
@@ -258,6 +267,72 @@ class Clusterer:
         if check and rc != TPX_OK:
             raise TpxError(rc, "tpx_cluster_run_host")
         return k.value
+
+
+class Pipeline:
+    """``tpx_pipeline_*``: overlap host<->device copies of one buffer with the
+    kernels of another (``depth`` slots, native worker threads).  Buffers are
+    CPU tensors (pinned) or numpy arrays and must stay alive until ``wait``."""
+
+    def __init__(self, dt_max: int, max_hits: int, capacity: int, depth: int = 2, width: int = 256,
+                 height: int = 256, variant: int = VARIANT_LOCAL):
+        torch = _torch()
+        proto = Clusterer(dt_max, width, height, variant)
+        b = ctypes.c_size_t(0)
+        _check(_pipe_ws(proto._h, int(max_hits), int(capacity), int(depth), ctypes.byref(b)),
+               "tpx_pipeline_workspace_bytes")
+        proto.close()
+        self._ws = torch.empty(max(b.value, 256), dtype=torch.uint8, device="cuda")
+        h = _vp()
+        _check(_pipe_create(int(dt_max), int(variant), int(width), int(height), int(max_hits), int(capacity),
+                            int(depth), self._ws.data_ptr(), self._ws.numel(), ctypes.byref(h)), "tpx_pipeline_create")
+        self._h = h
+        self._keep = {}
+
+    @staticmethod
+    def _ptr(a):
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+    @staticmethod
+    def _nbytes(a):
+        return a.numel() * a.element_size() if hasattr(a, "numel") else a.nbytes
+
+    def submit(self, hits_host, labels_host, features_host, capacity: int | None = None) -> int:
+        n = self._nbytes(hits_host) // 16
+        if capacity is None:
+            capacity = self._nbytes(features_host) // 64
+        t = _u64(0)
+        _check(_pipe_submit(self._h, self._ptr(hits_host), int(n), self._ptr(labels_host), self._ptr(features_host),
+                            int(capacity), ctypes.byref(t)), "tpx_pipeline_submit")
+        self._keep[t.value] = (hits_host, labels_host, features_host)
+        return t.value
+
+    def wait(self, ticket: int, check: bool = True) -> int:
+        k = _u64(0)
+        rc = _pipe_wait(self._h, int(ticket), ctypes.byref(k))
+        self._keep.pop(ticket, None)
+        if check:
+            _check(rc, "tpx_pipeline_wait")
+        return k.value
+
+    def mark(self, which: int):
+        _check(_pipe_mark(self._h, int(which)), "tpx_pipeline_mark")
+
+    def elapsed_ms(self) -> float:
+        ms = ctypes.c_float(0)
+        _check(_pipe_elapsed(self._h, ctypes.byref(ms)), "tpx_pipeline_elapsed_ms")
+        return ms.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _pipe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def centroids(features, stream=None):

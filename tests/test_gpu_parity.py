@@ -223,3 +223,26 @@ def test_full_size_sampled(tpx, preset):
         for name in pins.FEAT_FIELDS:
             assert int(row[name]) == int(f[name]), (seed, name)
     s.close()
+
+
+def test_pipeline_matches_run_host(tpx):
+    """tpx_pipeline_*: several buffers in flight give exactly run_host's results."""
+    bufs = [tpxgen.generate(p, n_hits=m, seed=s) for p, m, s in
+            (("mixed", 700_000, 11), ("lowflux", 300_000, 12), ("heavyion", 200_000, 13), ("mixed", 1_000_000, 14),
+             ("tiny", 10_000, 15))]
+    dts = {"mixed": 320, "lowflux": 320, "heavyion": 320, "tiny": 320}
+    pipe = tpx.Pipeline(320, max_hits=1_000_000, capacity=1_000_000, depth=3)
+    outs, tickets = [], []
+    for h in bufs:
+        hh = torch.from_numpy(h.view(np.uint8)).pin_memory()
+        lab = torch.empty(len(h), dtype=torch.int32).pin_memory()
+        ft = torch.empty((len(h), 64), dtype=torch.uint8).pin_memory()
+        outs.append((hh, lab, ft))
+        tickets.append(pipe.submit(hh, lab, ft))
+    for h, (hh, lab, ft), t in zip(bufs, outs, tickets):
+        k = pipe.wait(t)
+        rl, rf = oracle.cluster(h, 320)
+        assert k == len(rf)
+        assert np.array_equal(lab.numpy().view(np.uint32), rl)
+        assert tpx.features_to_numpy(ft[:k]).tobytes() == rf.tobytes()
+    pipe.close()
