@@ -33,9 +33,9 @@ namespace tpx {
 constexpr int kTileThreads = 256;
 constexpr int kTile = 1024;                    // tile hits per CTA
 constexpr int kHaloCap = 1024;                 // staged forward-halo hits
-constexpr int kBackCap = 512;                  // staged back-halo hits (openness only)
+constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
 constexpr int kFwdMax = kTile + kHaloCap;      // tile + forward halo (local index l)
-constexpr int kBuckets = 1024;                 // column buckets (x >> shift)
+constexpr int kBuckets = 1024;                 // one bucket per pixel column (wider sensors: global path)
 constexpr int kBucketCap = 512;                // longer buckets: the tile takes the global path
 constexpr int kStageItems = kFwdMax / kTileThreads;        // 8
 constexpr int kItemsPerThread = kTile / kTileThreads;      // 4
@@ -49,7 +49,6 @@ struct tile_args {
   uint64_t dt;
   uint32_t width;
   uint32_t n_owned;          // hits with input index >= n_owned carry no features (sharded halo)
-  uint32_t bucket_shift;     // bucket = x >> bucket_shift  (< kBuckets buckets)
   uint32_t* labels;          // labels_out (input order)
   uint32_t* parent_g;        // global union-find over sorted positions (open hits only)
   uint32_t* slot_of;         // root position -> stage slot (open components)
@@ -157,34 +156,33 @@ __device__ __forceinline__ void set_label_bit(uint32_t* bitmap, uint32_t label) 
 }
 
 // Shared-memory carve-up (bytes).  Region A holds the column index during the
-// clustering phase and the staged hits + member array during the reductions.
+// clustering phase and the staged hits + member array + labels afterwards.
 struct tile_smem_layout {
-  static constexpr size_t csort = 0;                                   // uint2 [kFwdMax]
-  static constexpr size_t csli = csort + (size_t)kFwdMax * 8;           // u16   [kFwdMax]
-  static constexpr size_t myrank = csli + (size_t)kFwdMax * 2;          // u16   [kFwdMax]
+  static constexpr size_t csort = 0;                                   // uint2 [kFwdMax] (toa - base, y<<16|x)
+  static constexpr size_t ckey = csort + (size_t)kFwdMax * 8;           // u32   [kFwdMax] y<<16 | local index
+  static constexpr size_t myrank = ckey + (size_t)kFwdMax * 4;          // u16   [kFwdMax]
   static constexpr size_t region_a = myrank + (size_t)kFwdMax * 2;
   // reduction-phase aliases of region A
   static constexpr size_t stile = 0;                                   // uint4 [kTile]
   static constexpr size_t mem = stile + (size_t)kTile * 16;             // u16   [kTile]
   static constexpr size_t big = mem + (size_t)kTile * 2;                // u16   [kTile]
-  static_assert(big + (size_t)kTile * 2 <= region_a, "reduction arrays alias region A");
-  static constexpr size_t hb = region_a;                                // uint2 [kHaloCap] (later: mlabel u32)
+  static constexpr size_t mlabel = big + (size_t)kTile * 2;             // u32   [kTile]
+  static_assert(mlabel + (size_t)kTile * 4 <= region_a, "reduction arrays alias region A");
+  static constexpr size_t hb = region_a;                                // uint2 [kBackCap]
   static constexpr size_t bs = hb + (size_t)kBackCap * 8;               // u32   [kBuckets + 4]
   static constexpr size_t par = bs + ((size_t)kBuckets + 4) * 4;        // u32   [kFwdMax]
-  static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile]
-  static constexpr size_t crank = csize + (size_t)kTile * 4;            // u16   [kTile]
+  static constexpr size_t cltmp = par;                                  // u32   [kFwdMax] (alias, before par)
+  static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile/2] (u16 pairs)
+  static constexpr size_t crank = csize + (size_t)kTile * 2;            // u16   [kTile]
   static constexpr size_t coff = crank + (size_t)kTile * 2;             // u16   [kTile]
   static constexpr size_t eb = coff + (size_t)kTile * 2;                // u16   [kEdgeBuf * threads]
-  static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2 > (size_t)kFwdMax * 2
-                                         ? (size_t)kEdgeBuf * kTileThreads * 2 : (size_t)kFwdMax * 2;
-  static constexpr size_t cltmp = eb;                                   // u16 [kFwdMax] (alias)
-  static constexpr size_t ccur = eb;                                    // u32 [kTile]   (alias)
+  static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2;
+  static constexpr size_t ccur = eb;                                    // u32   [kTile]   (alias)
   static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
   static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
   static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
   static constexpr size_t total = hflag + kTile;
 };
-static_assert((size_t)kTile * 4 <= (size_t)kBackCap * 8, "mlabel aliases the back halo");
 constexpr size_t kTileSmem = tile_smem_layout::total;
 constexpr uint32_t kBigComp = 24;  // components this large are reduced by a whole warp
 
@@ -262,20 +260,20 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
   using SL = tile_smem_layout;
   extern __shared__ __align__(16) unsigned char sm[];
   uint2* csort = reinterpret_cast<uint2*>(sm + SL::csort);      // (toa - base, y<<16|x), bucket-sorted
-  uint16_t* csli = reinterpret_cast<uint16_t*>(sm + SL::csli);  // local index of csort entries
+  uint32_t* ckey = reinterpret_cast<uint32_t*>(sm + SL::ckey);  // y << 16 | local index of csort entries
   uint16_t* myrank = reinterpret_cast<uint16_t*>(sm + SL::myrank);  // local index -> csort position
   uint4* stile = reinterpret_cast<uint4*>(sm + SL::stile);      // tile hits (toa - base, xy, tot, idx)
   uint16_t* mem = reinterpret_cast<uint16_t*>(sm + SL::mem);    // member array grouped by component
   uint16_t* big = reinterpret_cast<uint16_t*>(sm + SL::big);    // roots of large components
   uint2* hb = reinterpret_cast<uint2*>(sm + SL::hb);            // back halo, index order
-  uint32_t* mlabel = reinterpret_cast<uint32_t*>(sm + SL::hb);  // label by tile root (after the search)
+  uint32_t* mlabel = reinterpret_cast<uint32_t*>(sm + SL::mlabel);  // label by tile root (reductions)
   uint32_t* bs = reinterpret_cast<uint32_t*>(sm + SL::bs);      // bucket counts, then bucket starts
   uint32_t* par = reinterpret_cast<uint32_t*>(sm + SL::par);
-  uint32_t* csize = reinterpret_cast<uint32_t*>(sm + SL::csize);
+  uint32_t* csize2 = reinterpret_cast<uint32_t*>(sm + SL::csize);  // component sizes, two u16 per word
   uint16_t* crank = reinterpret_cast<uint16_t*>(sm + SL::crank);  // stage rank by root
   uint16_t* coff = reinterpret_cast<uint16_t*>(sm + SL::coff);    // member offset by root
   uint16_t* eb = reinterpret_cast<uint16_t*>(sm + SL::eb);
-  uint16_t* cltmp = reinterpret_cast<uint16_t*>(sm + SL::cltmp);
+  uint32_t* cltmp = reinterpret_cast<uint32_t*>(sm + SL::cltmp);
   uint32_t* ccur = reinterpret_cast<uint32_t*>(sm + SL::ccur);
   uint8_t* copen = sm + SL::copen;
   uint8_t* hflag = sm + SL::hflag;  // per tile hit: bit0 open mark, bit1 overflow
@@ -289,7 +287,6 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
   const uint64_t t1 = min(n, t0 + kTile);
   const uint32_t nt = (uint32_t)(t1 - t0);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t shift = a.bucket_shift;
   long long t_phase = clock64();
 
   // ---- halo ranges (32-ary warp searches in the sorted stream: warp 0 the
@@ -330,10 +327,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
   }
   for (uint32_t b = threadIdx.x; b < kBuckets + 4; b += kTileThreads) bs[b] = 0;
   for (uint32_t j = threadIdx.x; j < kTile; j += kTileThreads) {
-    csize[j] = 0;
     copen[j] = 0;
     hflag[j] = 0;
   }
+  for (uint32_t w = threadIdx.x; w < kTile / 2; w += kTileThreads) csize2[w] = 0;
   __syncthreads();
   TPX_PHASE(0);
   const uint64_t b0 = s_meta[0], f1 = s_meta[1], base = s_meta[2];
@@ -359,7 +356,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
       if (l < m) {
         const srec r = load_srec(S + t0 + l);
         ev[q] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-        eslot[q] = atomicAdd(bs + ((r.xy & 0xffffu) >> shift), 1u);
+        eslot[q] = atomicAdd(bs + (r.xy & 0xffffu), 1u);
       }
     }
   }
@@ -417,33 +414,43 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
     return;
   }
 
-  // ---- unordered scatter into buckets, then rank by time inside each bucket
+  // ---- unordered scatter into column buckets, then rank inside each bucket
+  // by (row, time): key = y << 16 | local index (local index order = ToA order)
 #pragma unroll
   for (int q = 0; q < kStageItems; ++q) {
     const uint32_t l = threadIdx.x + q * kTileThreads;
-    if (l < m) cltmp[bs[(ev[q].y & 0xffffu) >> shift] + eslot[q]] = (uint16_t)l;
+    if (l < m) cltmp[bs[ev[q].y & 0xffffu] + eslot[q]] = (ev[q].y & 0xffff0000u) | l;
   }
-  for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < kStageItems; ++q) {
     const uint32_t l = threadIdx.x + q * kTileThreads;
     if (l < m) {
-      const uint32_t b = (ev[q].y & 0xffffu) >> shift;
+      const uint32_t b = ev[q].y & 0xffffu;
+      const uint32_t key = (ev[q].y & 0xffff0000u) | l;
       const uint32_t s0 = bs[b], s1 = bs[b + 1];
       uint32_t r = 0;
-      for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < l;
+      for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < key;
       const uint32_t fin = s0 + r;
       csort[fin] = ev[q];
-      csli[fin] = (uint16_t)l;
+      ckey[fin] = key;
       myrank[l] = (uint16_t)fin;
     }
   }
   __syncthreads();
+  for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;  // par aliases cltmp
+  __syncthreads();
   TPX_PHASE(2);
 
-  // ---- window search over the 3 neighbouring column buckets (dynamic warp
-  // chunks; edges buffered, united after each chunk)
+  // ---- pixel-exact neighbour search.  For a hit at (x, y) with local index j
+  // only the FIRST later hit on each of its 9 neighbouring pixels needs an edge
+  // (later hits on that pixel are within dt of the first one and reach it via
+  // their own same-pixel edge; this is the paper's last-hit-per-pixel rule,
+  // P:171, read forwards).  Column x' in {x-1, x, x+1} is a bucket
+  // sorted by (row, time): one binary search finds row y-1 after j, then a
+  // short walk over rows y-1..y+1 takes the first entry per row with local
+  // index > j and tests it against dt.  Work per hit is independent of the
+  // window density (dense heavy-ion windows included).
   const uint64_t prev_last = s_meta[5];
   const uint64_t first_unstaged = s_meta[4];
   const uint32_t wmax = a.width - 1;
@@ -456,41 +463,28 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
     const uint32_t j = chunk * 32 + lane;
     uint32_t ne = 0;
     if (j < nt) {
-      const uint32_t pself = myrank[j];
-      const uint2 h = csort[pself];
-      const uint32_t x = h.y & 0xffffu;
-      const uint32_t bl = (x ? x - 1 : x) >> shift, bm = x >> shift, br = (x < wmax ? x + 1 : x) >> shift;
-      uint32_t seen = 0;  // neighbouring pixels (3x3 offsets) that already have their first later hit
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const uint32_t b = c == 0 ? bl : (c == 1 ? bm : br);
-        if ((c == 0 && b == bm) || (c == 2 && b == bm) || (c == 2 && b == bl)) continue;
-        uint32_t p, pe = bs[b + 1];
-        if (b == bm) {
-          p = pself + 1;
-        } else {  // first entry of the bucket with local index > j (entries are time-ordered)
-          uint32_t lo = bs[b], hi = pe;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (csli[mid] <= j) lo = mid + 1; else hi = mid;
-          }
-          p = lo;
+      const uint2 h = csort[myrank[j]];
+      const uint32_t x = h.y & 0xffffu, y = h.y >> 16;
+      const uint32_t xlo = x ? x - 1 : 0, xhi = x < wmax ? x + 1 : x;
+      const uint32_t ylo = y ? y - 1 : 0, yhi = y + 1;
+      const uint32_t k0 = (ylo << 16) | j;  // first key of interest: row ylo, index > j
+      for (uint32_t b = xlo; b <= xhi; ++b) {
+        uint32_t lo = bs[b], hi = bs[b + 1];
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (ckey[mid] <= k0) lo = mid + 1; else hi = mid;
         }
-        // Only the first later hit on each neighbouring pixel needs an edge:
-        // later hits on that pixel within the window are within dt of it and
-        // reach it through its own same-pixel edge ("window search").
-        for (; p < pe; ++p) {
-          const uint2 g = csort[p];
-          if (g.x - h.x > dt32) break;
-          const uint32_t d = g.y - h.y + 0x00010001u;  // (dy+1) << 16 | (dx+1) when adjacent
-          if (((d & 0xffffu) <= 2u) & ((d >> 16) <= 2u)) {
-            const uint32_t bit = 1u << ((d >> 16) * 3 + (d & 0xffffu));
-            if (!(seen & bit)) {
-              seen |= bit;
-              const uint32_t lj = csli[p];
-              if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
-              else s_unite(par, j, lj);
-            }
+        uint32_t taken = 0xffffffffu;  // row whose first later hit was already taken
+        for (uint32_t p = lo; p < bs[b + 1]; ++p) {
+          const uint32_t k = ckey[p];
+          const uint32_t row = k >> 16;
+          if (row > yhi) break;
+          if (row == taken || (k & 0xffffu) <= j) continue;
+          taken = row;
+          if (csort[p].x - h.x <= dt32) {
+            const uint32_t lj = k & 0xffffu;
+            if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
+            else s_unite(par, j, lj);
           }
         }
       }
@@ -536,7 +530,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
     const uint32_t r = j < nt ? par[j] : 0xffffffffu;
     const unsigned peers = __match_any_sync(kFull, r);
     if (j < nt) {
-      if ((__ffs(peers) - 1) == (int)lane) atomicAdd(&csize[r], (uint32_t)__popc(peers));
+      if ((__ffs(peers) - 1) == (int)lane) atomicAdd(csize2 + (r >> 1), (uint32_t)__popc(peers) << ((r & 1) * 16));
       if (hflag[j] & 1u) copen[r] = 1;
       rq[q] = load_srec(S + t0 + j);
       stile[j] = make_uint4((uint32_t)(srec_toa(rq[q]) - base), rq[q].xy, srec_tot(rq[q]), rq[q].idx);
@@ -569,7 +563,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
       const uint32_t j = threadIdx.x * kItemsPerThread + q;  // blocked for rank order
       uint32_t v = 0;
       if (j < nt && par[j] == j) {
-        const uint32_t sz = csize[j];
+        const uint32_t sz = (csize2[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
         v = 1u | ((sz >= 2 ? sz : 0u) << 16);
       }
       packed[q] = v;
@@ -597,7 +591,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
     const uint32_t j = threadIdx.x + q * kTileThreads;
     if (j < nt) {
       const uint32_t r = par[j];
-      if (csize[r] >= 2) mem[coff[r] + atomicAdd(&ccur[r], 1u)] = (uint16_t)j;
+      if (((csize2[r >> 1] >> ((r & 1) * 16)) & 0xffffu) >= 2) mem[coff[r] + atomicAdd(&ccur[r], 1u)] = (uint16_t)j;
     }
   }
   __syncthreads();
@@ -609,7 +603,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
   for (int q = 0; q < kItemsPerThread; ++q) {
     const uint32_t j = threadIdx.x + q * kTileThreads;
     if (j < nt && par[j] == j) {
-      const uint32_t sz = csize[j];
+      const uint32_t sz = (csize2[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
       if (sz < kBigComp) {
         feat_acc f;
         f.init();
@@ -630,7 +624,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
     if (lane == 0) bi = atomicAdd(&s_bigq, 1u);
     bi = __shfl_sync(kFull, bi, 0);
     if (bi >= s_nbig) break;
-    const uint32_t r = big[bi], sz = csize[r], o = coff[r];
+    const uint32_t r = big[bi], sz = (csize2[r >> 1] >> ((r & 1) * 16)) & 0xffffu, o = coff[r];
     feat_acc f;
     f.init();
     for (uint32_t k = lane; k < sz; k += 32) f.add(stile[mem[o + k]], a.n_owned);

@@ -269,8 +269,6 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.dt = c->dt;
   a.width = c->width;
   a.n_owned = (uint32_t)r.n_owned;
-  a.bucket_shift = 0;
-  while (((c->width - 1) >> a.bucket_shift) >= (uint32_t)kBuckets) ++a.bucket_shift;
   a.labels = r.labels;
   a.parent_g = parent_g;
   a.slot_of = slot_of;
@@ -475,7 +473,9 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     }
     c->stats.sort_path = attempt >= 2 ? 1 : 0;
     c->stats.sort_retries = attempt < 2 ? attempt : 2;
-    rc = attempt == 3 ? cluster_global(c, r) : cluster_sorted(c, r);
+    // the tile kernel indexes one bucket per pixel column: wider sensors take
+    // the global union-find pipeline
+    rc = (attempt == 3 || c->width > (uint32_t)kBuckets) ? cluster_global(c, r) : cluster_sorted(c, r);
     if (rc) return rc;
     if ((rc = read_header(c, r))) return rc;
     const dev_hdr& h = *c->host_hdr;
