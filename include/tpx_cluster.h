@@ -182,6 +182,9 @@ typedef struct tpx_run_stats {
   uint64_t overflow_hits;  /* hits whose ToA window left the staged halo     */
   uint64_t tile_phase_cycles[16]; /* tile-kernel phase clocks, summed over
                               CTAs (only when profiling; diagnostics)        */
+  uint32_t tile_dense;     /* 1 if the dense (large-halo) tile configuration
+                              ran (window-density probe)                     */
+  uint32_t reserved0;
 } tpx_run_stats;
 
 int tpx_cluster_last_stats(const tpx_cluster* ctx, tpx_run_stats* out);
@@ -190,6 +193,13 @@ int tpx_cluster_last_stats(const tpx_cluster* ctx, tpx_run_stats* out);
  * (events are recorded on the run stream; adds no synchronisation beyond the
  * run's own final sync). */
 int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
+
+/* Tile configuration of the clustering kernel: TPX_TILE_AUTO (default) lets
+ * a window-density probe on the sorted stream choose; TPX_TILE_SPARSE /
+ * TPX_TILE_DENSE force one (results are identical; only speed differs --
+ * used by the parity tests to cover both).  Errors: INVALID_ARG. */
+enum { TPX_TILE_AUTO = 0, TPX_TILE_SPARSE = 1, TPX_TILE_DENSE = 2 };
+int tpx_cluster_set_tile_mode(tpx_cluster* ctx, int mode);
 
 /* Static name of stage i (0 <= i < 16) as reported in stage_ms; "" if unused. */
 const char* tpx_cluster_stage_name(int i);

@@ -44,6 +44,7 @@ class RunStats(ctypes.Structure):
         ("cross_pairs", _u64), ("kernel_launches", _u32), ("n_stages", _u32),
         ("stage_ms", ctypes.c_float * 16),
         ("open_hits", _u64), ("overflow_hits", _u64), ("tile_phase_cycles", _u64 * 16),
+        ("tile_dense", _u32), ("reserved0", _u32),
     ]
 
 
@@ -68,6 +69,8 @@ _run_host = _proto("tpx_cluster_run_host", _int, _vp, _vp, _u64, _vp, _vp, _u64,
 _centroids = _proto("tpx_cluster_centroids", _int, _vp, _u64, _vp, _vp)
 _last_stats = _proto("tpx_cluster_last_stats", _int, _vp, ctypes.POINTER(RunStats))
 _set_profiling = _proto("tpx_cluster_set_profiling", _int, _vp, _int)
+_set_tile_mode = _proto("tpx_cluster_set_tile_mode", _int, _vp, _int)
+TILE_MODES = {"auto": 0, "sparse": 1, "dense": 2}
 _stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
 _run_partial = _proto("tpx_cluster_run_partial", _int, _vp, _vp, _u64, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
                       _vp, ctypes.c_size_t, _vp)
@@ -192,6 +195,10 @@ class Clusterer:
 
     def set_profiling(self, on: bool = True):
         _set_profiling(self._h, 1 if on else 0)
+
+    def set_tile_mode(self, mode: str = "auto"):
+        """'auto' (density probe), 'sparse' or 'dense' tile configuration."""
+        _check(_set_tile_mode(self._h, TILE_MODES[mode]), "tpx_cluster_set_tile_mode")
 
     def stats(self) -> dict:
         s = RunStats()

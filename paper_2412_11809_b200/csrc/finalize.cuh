@@ -16,26 +16,44 @@ constexpr int kListGrid = 148 * 8;
 __device__ __forceinline__ void flag_internal(dev_hdr* hdr) { atomicOr(&hdr->err, 2u); }
 
 // Hits whose forward window left the staged halo: scan the rest of the window
-// in global memory (any j it reaches belongs to an open component).
+// in global memory, one warp per hit (lane = candidate, 32 per step); any j it
+// reaches belongs to an open component.
 __global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __restrict__ S, uint64_t n, uint64_t dt,
                                                                   const uint32_t* __restrict__ list, dev_hdr* hdr,
                                                                   uint32_t* parent_g) {
   const uint64_t cnt = hdr->n_overflow;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (uint64_t)gridDim.x * blockDim.x) {
+  const unsigned lane = lane_id();
+  const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t t = wid; t < cnt; t += nw) {
     const uint32_t i = list[t];
     const srec a = load_srec(S + i);
     const uint64_t ta = srec_toa(a);
-    for (uint64_t j = (uint64_t)i + 1; j < n; ++j) {
-      const srec b = load_srec(S + j);
-      if (srec_toa(b) - ta > dt) break;
-      if (adjacent(a.xy, b.xy)) {
-        if (ld_cg(parent_g + j) == kSentinel) {
-          flag_internal(hdr);
-          return;
-        }
-        uf_unite(parent_g, i, (uint32_t)j);
+    for (uint64_t j0 = (uint64_t)i + 1; j0 < n; j0 += 32) {
+      const uint64_t j = j0 + lane;
+      bool in = false, adj = false;
+      if (j < n) {
+        const srec b = load_srec(S + j);
+        in = srec_toa(b) - ta <= dt;
+        adj = in && adjacent(a.xy, b.xy);
       }
+      if (adj) {
+        if (ld_cg(parent_g + j) == kSentinel) flag_internal(hdr);
+        else uf_unite(parent_g, i, (uint32_t)j);
+      }
+      if (!__all_sync(kFull, in)) break;  // past the window (sorted by ToA)
     }
+  }
+}
+
+// After all unions: parent_g[pos] <- root for every open hit (read-only walk;
+// every stored value is a final root), so later lookups are one load.
+__global__ void __launch_bounds__(kListThreads) k_flatten_open(const uint32_t* __restrict__ open_hits, dev_hdr* hdr,
+                                                               uint32_t* parent_g) {
+  const uint64_t nh = hdr->n_open_hits;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t pos = open_hits[t];
+    parent_g[pos] = uf_root(parent_g, pos);
   }
 }
 
@@ -60,7 +78,7 @@ __global__ void __launch_bounds__(kListThreads) k_merge_open(const uint32_t* __r
   const uint64_t cnt = hdr->n_open_comps;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t r = open_comps[t];
-    const uint32_t R = uf_root(parent_g, r);
+    const uint32_t R = parent_g[r];  // flattened
     if (R == r) continue;
     tpx_cluster_features* src = stage + slot_of[r];
     tpx_cluster_features* dst = stage + slot_of[R];
@@ -91,16 +109,32 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh; t += stride) {
     const uint32_t pos = open_hits[t];
-    const uint32_t R = uf_root(parent_g, pos);
-    labels[S[pos].idx] = stage[slot_of[R]].label;
+    labels[S[pos].idx] = stage[slot_of[parent_g[pos]]].label;  // flattened
   }
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += stride) {
     const uint32_t r = open_comps[t];
-    if (uf_root(parent_g, r) == r) {
+    if (parent_g[r] == r) {
       const uint32_t lab = stage[slot_of[r]].label;
       if (lab < n_owned) set_label_bit(bitmap, lab);
     }
   }
+}
+
+// Window-density probe on the sorted stream: for 128 evenly spaced hits, the
+// number of later hits within dt_max (binary search).  The host uses it to
+// pick the tile configuration (tile_cc.cuh: tile_sparse / tile_dense).
+constexpr int kProbeSamples = 128;
+__global__ void k_density_probe(const srec* __restrict__ S, uint64_t n, uint64_t dt, uint32_t* __restrict__ out) {
+  const uint32_t k = threadIdx.x;
+  if (k >= kProbeSamples) return;
+  const uint64_t p = (n - 1) * k / (kProbeSamples - 1);
+  const uint64_t t = srec_key_toa(S, p);
+  uint64_t lo = p + 1, hi = p + (1ull << 16) < n ? p + (1ull << 16) : n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (srec_key_toa(S, mid) <= t + dt) lo = mid + 1; else hi = mid;
+  }
+  out[k] = (uint32_t)(lo - p - 1);
 }
 
 __global__ void k_popc(const uint32_t* __restrict__ bitmap, uint64_t nwords, uint32_t* __restrict__ cnt) {

@@ -32,16 +32,28 @@ namespace tpx {
 
 constexpr int kTileThreads = 256;
 constexpr int kTile = 1024;                    // tile hits per CTA
-constexpr int kHaloCap = 1024;                 // staged forward-halo hits
 constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
-constexpr int kFwdMax = kTile + kHaloCap;      // tile + forward halo (local index l)
 constexpr int kBuckets = 1024;                 // one bucket per pixel column (wider sensors: global path)
 constexpr int kBucketCap = 512;                // longer buckets: the tile takes the global path
-constexpr int kStageItems = kFwdMax / kTileThreads;        // 8
 constexpr int kItemsPerThread = kTile / kTileThreads;      // 4
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and chunk
-static_assert(kFwdMax % kTileThreads == 0, "staging layout");
+
+// Tile configurations: the forward halo must hold the hits within dt_max of
+// the tile's last hit.  Sparse streams (windows of tens of hits) use a 1024
+// halo and fit 4 CTAs per SM; dense heavy-ion streams (windows of ~1-3k hits,
+// SURVEY H1) use a 3072 halo at 2 CTAs per SM so that windows stay on chip.
+template <int kHaloHits, int kMinBlocks>
+struct tile_cfg {
+  static constexpr int kHalo = kHaloHits;
+  static constexpr int kFwdMax = kTile + kHaloHits;               // tile + forward halo (local index l)
+  static constexpr int kStageItems = kFwdMax / kTileThreads;
+  static constexpr bool kRegStage = kStageItems <= 8;             // stage in registers, else re-read S
+  static constexpr int kBlocks = kMinBlocks;
+  static_assert(kFwdMax % kTileThreads == 0, "staging layout");
+};
+using tile_sparse = tile_cfg<1024, 4>;
+using tile_dense = tile_cfg<3072, 2>;
 
 struct tile_args {
   const srec* S;
@@ -157,7 +169,9 @@ __device__ __forceinline__ void set_label_bit(uint32_t* bitmap, uint32_t label) 
 
 // Shared-memory carve-up (bytes).  Region A holds the column index during the
 // clustering phase and the staged hits + member array + labels afterwards.
+template <class C>
 struct tile_smem_layout {
+  static constexpr size_t kFwdMax = C::kFwdMax;
   static constexpr size_t csort = 0;                                   // uint2 [kFwdMax] (toa - base, y<<16|x)
   static constexpr size_t ckey = csort + (size_t)kFwdMax * 8;           // u32   [kFwdMax] y<<16 | local index
   static constexpr size_t myrank = ckey + (size_t)kFwdMax * 4;          // u16   [kFwdMax]
@@ -181,9 +195,13 @@ struct tile_smem_layout {
   static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
   static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
   static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
-  static constexpr size_t total = hflag + kTile;
+  static constexpr size_t eslot = hflag + kTile;                       // u16   [kFwdMax] (dense staging)
+  static constexpr size_t total = eslot + (C::kRegStage ? 0 : (size_t)kFwdMax * 2);
 };
-constexpr size_t kTileSmem = tile_smem_layout::total;
+template <class C>
+constexpr size_t tile_smem_bytes() {
+  return tile_smem_layout<C>::total;
+}
 constexpr uint32_t kBigComp = 24;  // components this large are reduced by a whole warp
 
 // Block-wide exclusive scan (kTileThreads threads) of one u32 per thread.
@@ -256,8 +274,11 @@ struct feat_acc {
   }
 };
 
-__global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
-  using SL = tile_smem_layout;
+template <class C>
+__global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args a) {
+  using SL = tile_smem_layout<C>;
+  constexpr int kFwdMax = C::kFwdMax;
+  constexpr int kStageItems = C::kStageItems;
   extern __shared__ __align__(16) unsigned char sm[];
   uint2* csort = reinterpret_cast<uint2*>(sm + SL::csort);      // (toa - base, y<<16|x), bucket-sorted
   uint32_t* ckey = reinterpret_cast<uint32_t*>(sm + SL::ckey);  // y << 16 | local index of csort entries
@@ -309,7 +330,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
     }
   } else if (warp == 1) {
     const uint64_t toa_last = srec_key_toa(S, t1 - 1);
-    const uint64_t flim = min(n, t1 + kHaloCap);
+    const uint64_t flim = min(n, t1 + (uint64_t)C::kHalo);
     // forward halo: first position with toa > toa_last + dt
     const uint64_t f1 = warp_lower_bound(t1, flim, [&](uint64_t p) { return srec_key_toa(S, p) > toa_last + dt; });
     if (lane == 0) {
@@ -343,21 +364,33 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
   const uint32_t dt32 = dt > 0xffffffffull ? 0xffffffffu : (uint32_t)dt;  // rel. ToAs differ by < 2^32
 
   // ---- stage: back halo, and tile + forward halo counted into column buckets
-  uint2 ev[kStageItems];
-  uint32_t eslot[kStageItems];
+  // (sparse config: the 8 staged words per thread stay in registers; dense
+  // config: slots go to shared memory and S is re-read from L2)
+  constexpr int kRegItems = C::kRegStage ? kStageItems : 1;
+  uint2 ev[kRegItems];
+  uint32_t eslot[kRegItems];
+  uint16_t* eslot_s = reinterpret_cast<uint16_t*>(sm + SL::eslot);
+  auto staged = [&](uint32_t l) {
+    const srec r = load_srec(S + t0 + l);
+    return make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
+  };
   if (!wide) {
     for (uint32_t k = threadIdx.x; k < nb; k += kTileThreads) {
       const srec r = load_srec(S + b0 + k);
       hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
     }
+    if constexpr (C::kRegStage) {
 #pragma unroll
-    for (int q = 0; q < kStageItems; ++q) {
-      const uint32_t l = threadIdx.x + q * kTileThreads;
-      if (l < m) {
-        const srec r = load_srec(S + t0 + l);
-        ev[q] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-        eslot[q] = atomicAdd(bs + (r.xy & 0xffffu), 1u);
+      for (int q = 0; q < kStageItems; ++q) {
+        const uint32_t l = threadIdx.x + q * kTileThreads;
+        if (l < m) {
+          ev[q] = staged(l);
+          eslot[q] = atomicAdd(bs + (ev[q].y & 0xffffu), 1u);
+        }
       }
+    } else {
+      for (uint32_t l = threadIdx.x; l < m; l += kTileThreads)
+        eslot_s[l] = (uint16_t)atomicAdd(bs + (staged(l).y & 0xffffu), 1u);
     }
   }
   __syncthreads();
@@ -416,26 +449,36 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile_cc(tile_args a) {
 
   // ---- unordered scatter into column buckets, then rank inside each bucket
   // by (row, time): key = y << 16 | local index (local index order = ToA order)
+  auto rank_in_bucket = [&](uint32_t l, uint2 e) {
+    const uint32_t b = e.y & 0xffffu;
+    const uint32_t key = (e.y & 0xffff0000u) | l;
+    const uint32_t s0 = bs[b], s1 = bs[b + 1];
+    uint32_t r = 0;
+    for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < key;
+    const uint32_t fin = s0 + r;
+    csort[fin] = e;
+    ckey[fin] = key;
+    myrank[l] = (uint16_t)fin;
+  };
+  if constexpr (C::kRegStage) {
 #pragma unroll
-  for (int q = 0; q < kStageItems; ++q) {
-    const uint32_t l = threadIdx.x + q * kTileThreads;
-    if (l < m) cltmp[bs[ev[q].y & 0xffffu] + eslot[q]] = (ev[q].y & 0xffff0000u) | l;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < kStageItems; ++q) {
-    const uint32_t l = threadIdx.x + q * kTileThreads;
-    if (l < m) {
-      const uint32_t b = ev[q].y & 0xffffu;
-      const uint32_t key = (ev[q].y & 0xffff0000u) | l;
-      const uint32_t s0 = bs[b], s1 = bs[b + 1];
-      uint32_t r = 0;
-      for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < key;
-      const uint32_t fin = s0 + r;
-      csort[fin] = ev[q];
-      ckey[fin] = key;
-      myrank[l] = (uint16_t)fin;
+    for (int q = 0; q < kStageItems; ++q) {
+      const uint32_t l = threadIdx.x + q * kTileThreads;
+      if (l < m) cltmp[bs[ev[q].y & 0xffffu] + eslot[q]] = (ev[q].y & 0xffff0000u) | l;
     }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kStageItems; ++q) {
+      const uint32_t l = threadIdx.x + q * kTileThreads;
+      if (l < m) rank_in_bucket(l, ev[q]);
+    }
+  } else {
+    for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
+      const uint2 e = staged(l);
+      cltmp[bs[e.y & 0xffffu] + eslot_s[l]] = (e.y & 0xffff0000u) | l;
+    }
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) rank_in_bucket(l, staged(l));
   }
   __syncthreads();
   for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;  // par aliases cltmp

@@ -89,6 +89,7 @@ struct tpx_cluster {
   uint32_t width, height;
   dev_hdr* host_hdr;  // pinned
   int profiling;
+  int tile_mode;  // TPX_TILE_*
   cudaEvent_t ev[kMaxStages + 1];
   tpx_run_stats stats;
   int cuda_ready;  // CUDA resources are created lazily by the first run
@@ -121,7 +122,10 @@ static int ensure_cuda(tpx_cluster* c) {
                            (int)window_sort_smem<12>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_window_sort<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_smem<24>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tile_cc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem) != cudaSuccess)
+      cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tile_cc<tile_dense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tile_smem_bytes<tile_dense>()) != cudaSuccess)
     return TPX_ERR_CUDA;
   if (cudaMallocHost(&c->host_hdr, sizeof(dev_hdr)) != cudaSuccess) return TPX_ERR_CUDA;
   for (int i = 0; i <= kMaxStages; ++i) {
@@ -203,6 +207,7 @@ struct run_ptrs {
   char* ws;
   layout L;
   cudaStream_t s;
+  bool dense;  // tile configuration chosen by the density probe
 };
 
 static int reset_header(tpx_cluster* c, const run_ptrs& r) {
@@ -282,13 +287,18 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.hdr = hdr;
   a.verify_stride = kWSortTile;
   a.phase_cycles = c->profiling ? hdr->phase_cycles : nullptr;
-  k_tile_cc<<<L.tiles, kTileThreads, kTileSmem, r.s>>>(a);
+  if (r.dense)
+    k_tile_cc<tile_dense><<<L.tiles, kTileThreads, tile_smem_bytes<tile_dense>(), r.s>>>(a);
+  else
+    k_tile_cc<tile_sparse><<<L.tiles, kTileThreads, tile_smem_bytes<tile_sparse>(), r.s>>>(a);
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[2], r.s);
   k_overflow_unions<<<kListGrid, kListThreads, 0, r.s>>>(S, r.n, c->dt, overflow, hdr, parent_g);
   TPX_LAUNCHED(c);
   k_pair_unions<<<kListGrid, kListThreads, 0, r.s>>>(pairs, hdr, parent_g);
+  TPX_LAUNCHED(c);
+  k_flatten_open<<<kListGrid, kListThreads, 0, r.s>>>(open_hits, hdr, parent_g);
   TPX_LAUNCHED(c);
   k_merge_open<<<kListGrid, kListThreads, 0, r.s>>>(open_comps, hdr, parent_g, slot_of, stage);
   TPX_LAUNCHED(c);
@@ -411,6 +421,12 @@ int tpx_cluster_set_profiling(tpx_cluster* c, int enable) {
   return TPX_OK;
 }
 
+int tpx_cluster_set_tile_mode(tpx_cluster* c, int mode) {
+  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_DENSE) return TPX_ERR_INVALID_ARG;
+  c->tile_mode = mode;
+  return TPX_OK;
+}
+
 int tpx_cluster_last_stats(const tpx_cluster* c, tpx_run_stats* out) {
   if (!c || !out) return TPX_ERR_INVALID_ARG;
   *out = c->stats;
@@ -472,6 +488,23 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       if ((rc = sort_global(c, r))) return rc;
     }
     c->stats.sort_path = attempt >= 2 ? 1 : 0;
+    // window-density probe (one small read-back): dense heavy-ion windows use
+    // the large-halo tile configuration
+    if (c->tile_mode != TPX_TILE_AUTO) {
+      r.dense = c->tile_mode == TPX_TILE_DENSE;
+      c->stats.tile_dense = r.dense ? 1 : 0;
+    } else {
+      uint32_t* probe = (uint32_t*)(r.ws + r.L.wcnt);  // scratch: wcnt is rewritten by k_popc later
+      k_density_probe<<<1, kProbeSamples, 0, r.s>>>(S, n, c->dt, probe);
+      TPX_LAUNCHED(c);
+      uint32_t hprobe[kProbeSamples];
+      TPX_CUDA(cudaMemcpyAsync(hprobe, probe, sizeof(hprobe), cudaMemcpyDeviceToHost, r.s));
+      TPX_CUDA(cudaStreamSynchronize(r.s));
+      int big = 0;
+      for (int i = 0; i < kProbeSamples; ++i) big += hprobe[i] > (uint32_t)(tile_sparse::kHalo * 5 / 8);
+      r.dense = big * 10 > kProbeSamples;  // > 10 % of the samples have windows near the sparse halo
+      c->stats.tile_dense = r.dense ? 1 : 0;
+    }
     c->stats.sort_retries = attempt < 2 ? attempt : 2;
     // the tile kernel indexes one bucket per pixel column: wider sensors take
     // the global union-find pipeline

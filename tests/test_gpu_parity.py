@@ -30,10 +30,11 @@ def tpx():
 _ctx_cache = {}
 
 
-def _gpu(tpx, h, dt, W=256, H=256, capacity=None):
-    key = (dt, W, H)
+def _gpu(tpx, h, dt, W=256, H=256, capacity=None, tile_mode="auto"):
+    key = (dt, W, H, tile_mode)
     if key not in _ctx_cache:
         _ctx_cache[key] = tpx.Clusterer(dt, W, H)
+        _ctx_cache[key].set_tile_mode(tile_mode)
     c = _ctx_cache[key]
     n = len(h)
     d = torch.from_numpy(np.ascontiguousarray(h).view(np.uint8).reshape(-1)).cuda() if n else \
@@ -45,8 +46,8 @@ def _gpu(tpx, h, dt, W=256, H=256, capacity=None):
             cxy.cpu().numpy(), c.stats())
 
 
-def _assert_parity(tpx, h, dt, W=256, H=256, ctx=""):
-    gl, gf, k, gc, st = _gpu(tpx, h, dt, W, H)
+def _assert_parity(tpx, h, dt, W=256, H=256, ctx="", tile_mode="auto"):
+    gl, gf, k, gc, st = _gpu(tpx, h, dt, W, H, tile_mode=tile_mode)
     rl, rf = oracle.cluster(h, dt, W, H)
     assert k == len(rf), f"{ctx}: n_clusters {k} vs {len(rf)}"
     bad = np.nonzero(gl != rl)[0]
@@ -105,6 +106,34 @@ def test_presets(tpx, preset, n):
     h = tpxgen.generate(preset, n_hits=n)
     W, H = (448, 512) if preset == "timepix4" else (256, 256)
     _assert_parity(tpx, h, p["dt_max"], W, H, ctx=preset)
+
+
+@pytest.mark.parametrize("mode", ["sparse", "dense"])
+@pytest.mark.parametrize("preset,n", [("mixed", 1_000_000), ("heavyion", 1_000_000), ("lowflux", 500_000)])
+def test_forced_tile_modes(tpx, mode, preset, n):
+    """Both tile configurations give the oracle's result on every workload
+    (the density probe only chooses the faster one)."""
+    h = tpxgen.generate(preset, n_hits=n)
+    st = _assert_parity(tpx, h, tpxgen.PRESETS[preset]["dt_max"], ctx=f"{preset}/{mode}", tile_mode=mode)
+    assert st["tile_dense"] == (mode == "dense")
+
+
+def test_forced_dense_small_and_fuzz(tpx):
+    rng = np.random.default_rng(77)
+    for trial in range(40):
+        W, H = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        dt = int(rng.choice([0, 3, 128]))
+        h = tpxgen.random_small(rng, int(rng.integers(1, 5000)), W, H, max(4 * dt, 3))
+        _assert_parity(tpx, h, dt, W, H, ctx=f"dense trial {trial}", tile_mode="dense")
+    for n in (4095, 4097, 65537):
+        _assert_parity(tpx, tpxgen.generate("mixed", n_hits=n), 320, ctx=f"dense n={n}", tile_mode="dense")
+
+
+def test_density_probe_choice(tpx):
+    _, _, _, _, st = _gpu(tpx, tpxgen.generate("heavyion", n_hits=2_000_000), 64)
+    assert st["tile_dense"] == 1
+    _, _, _, _, st = _gpu(tpx, tpxgen.generate("lowflux", n_hits=2_000_000), 128)
+    assert st["tile_dense"] == 0
 
 
 def test_lowflux_full_config(tpx):
