@@ -156,6 +156,28 @@ def run_reference(args):
     return 0
 
 
+def _e2e(tpx, dt, n, h_host, lab_host, feat_host, cap_host, depth, e2e_steps):
+    pipe = tpx.Pipeline(dt, max_hits=n, capacity=cap_host, depth=depth)
+
+    def run_pipe(nsteps):
+        tickets, ks = [], []
+        for i in range(nsteps):
+            if len(tickets) >= depth:
+                ks.append(pipe.wait(tickets.pop(0)))
+            tickets.append(pipe.submit(h_host, lab_host[i % depth], feat_host[i % depth], capacity=cap_host))
+        while tickets:
+            ks.append(pipe.wait(tickets.pop(0)))
+        return ks
+
+    run_pipe(depth)  # warm-up
+    pipe.mark(0)
+    ks = run_pipe(e2e_steps)
+    pipe.mark(1)
+    e2e_ms = pipe.elapsed_ms() / e2e_steps
+    pipe.close()
+    return e2e_ms, ks[-1]
+
+
 def run_ours(args):
     import torch
 
@@ -213,32 +235,17 @@ def run_ours(args):
     # paper's stream overlap); every step copies its 3.2 GB of
     # hits in and its labels + records out inside the timed region
     cap_host = max(n // 4, 1)
-    depth = 3
+    depth = 0 if args.no_e2e else 3
     lab_host = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(depth)]
     feat_host = [torch.empty((cap_host, 64), dtype=torch.uint8).pin_memory() for _ in range(depth)]
     del wsbuf, labels, feats
     torch.cuda.empty_cache()
-    pipe = tpx.Pipeline(dt, max_hits=n, capacity=cap_host, depth=depth)
     e2e_steps = max(2, min(args.steps, 6))
+    e2e_ms, kk = float("nan"), k
+    if depth:
+        e2e_ms, kk = _e2e(tpx, dt, n, h_host, lab_host, feat_host, cap_host, depth, e2e_steps)
 
-    def run_pipe(nsteps):
-        tickets, ks = [], []
-        for i in range(nsteps):
-            if len(tickets) >= depth:
-                ks.append(pipe.wait(tickets.pop(0)))
-            tickets.append(pipe.submit(h_host, lab_host[i % depth], feat_host[i % depth], capacity=cap_host))
-        while tickets:
-            ks.append(pipe.wait(tickets.pop(0)))
-        return ks
 
-    run_pipe(depth)  # warm-up
-    pipe.mark(0)
-    ks = run_pipe(e2e_steps)
-    pipe.mark(1)
-    e2e_ms = pipe.elapsed_ms() / e2e_steps
-    kk = ks[-1]
-    pipe.close()
-    del pipe
 
     # ---- roofline of the dominant kernel (B_alg = 16 + 4 + 64/s_bar per hit)
     s_bar = n / max(k, 1)
@@ -426,6 +433,7 @@ def main():
     ap.add_argument("--ref-step-sample", type=int, default=4_000_000,
                     help="hits per --impl reference step (~3.5 s of single-threaded CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -189,9 +189,10 @@ typedef struct tpx_run_stats {
 
 int tpx_cluster_last_stats(const tpx_cluster* ctx, tpx_run_stats* out);
 
-/* Enable (1) / disable (0) per-stage CUDA-event timing inside tpx_cluster_run
- * (events are recorded on the run stream; adds no synchronisation beyond the
- * run's own final sync). */
+/* 0: off.  1: per-stage CUDA-event timing inside tpx_cluster_run (events are
+ * recorded on the run stream; adds no synchronisation beyond the run's own
+ * final sync).  2: also per-phase clock counters inside the tile kernel
+ * (diagnostics; slows the kernel).  Errors: INVALID_ARG. */
 int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
 
 /* Tile configuration of the clustering kernel: TPX_TILE_AUTO (default) lets

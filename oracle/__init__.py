@@ -33,6 +33,13 @@ FEAT_DTYPE = np.dtype(
 )
 assert FEAT_DTYPE.itemsize == 64
 
+#: 32-byte shape record (the layout of tpx_cluster_shape).
+SHAPE_DTYPE = np.dtype(
+    [("x_min", "<u2"), ("x_max", "<u2"), ("y_min", "<u2"), ("y_max", "<u2"),
+     ("sum_xx", "<u8"), ("sum_xy", "<u8"), ("sum_yy", "<u8")]
+)
+assert SHAPE_DTYPE.itemsize == 32
+
 LOCAL, GLOBAL, STATIC = 0, 1, 2
 
 
@@ -70,6 +77,10 @@ def _load():
         L.oracle_index_component.restype = ctypes.c_int64
         L.oracle_cluster_streaming.argtypes = [vp, u64, u64, u32, u32, ctypes.c_int, vp]
         L.oracle_cluster_streaming.restype = ctypes.c_int
+        L.oracle_shapes.argtypes = [vp, u64, vp, vp, u64, vp]
+        L.oracle_shapes.restype = ctypes.c_int
+        L.oracle_group.argtypes = [vp, u64, vp, vp, u64, vp, vp, vp]
+        L.oracle_group.restype = ctypes.c_int
         L.oracle_centroids.argtypes = [vp, u64, vp]
         L.oracle_centroids.restype = None
         _lib = L
@@ -119,6 +130,40 @@ def cluster_streaming(hits, dt: int, variant: int, width: int = 256, height: int
     if rc != 0:
         raise OracleError(f"oracle_cluster_streaming returned {rc}")
     return labels
+
+
+def shapes(hits, labels, feats) -> np.ndarray:
+    """Bounding box + unweighted second moments per cluster (order of feats)."""
+    h = _hits(hits)
+    lab = np.ascontiguousarray(labels, dtype=np.uint32)
+    f = np.ascontiguousarray(feats, dtype=FEAT_DTYPE)
+    out = np.zeros(max(len(f), 1), dtype=SHAPE_DTYPE)
+    rc = _load().oracle_shapes(h.ctypes.data if len(h) else None, len(h), lab.ctypes.data if len(h) else None,
+                               f.ctypes.data if len(f) else None, len(f), out.ctypes.data)
+    if rc != 0:
+        raise OracleError(f"oracle_shapes returned {rc}")
+    return out[: len(f)].copy()
+
+
+def group(hits, labels, feats):
+    """Cluster-contiguous order (Alg. GPU Step 6, reading R18).
+
+    Returns ``(order uint32[n], offsets uint64[k+1], cluster_of uint32[k])``.
+    """
+    h = _hits(hits)
+    n = len(h)
+    lab = np.ascontiguousarray(labels, dtype=np.uint32)
+    f = np.ascontiguousarray(feats, dtype=FEAT_DTYPE)
+    k = len(f)
+    order = np.zeros(max(n, 1), dtype=np.uint32)
+    offsets = np.zeros(k + 1, dtype=np.uint64)
+    cof = np.zeros(max(k, 1), dtype=np.uint32)
+    rc = _load().oracle_group(h.ctypes.data if n else None, n, lab.ctypes.data if n else None,
+                              f.ctypes.data if k else None, k, order.ctypes.data, offsets.ctypes.data,
+                              cof.ctypes.data)
+    if rc != 0:
+        raise OracleError(f"oracle_group returned {rc}")
+    return order[:n].copy(), offsets, cof[:k].copy()
 
 
 def centroids(feats) -> np.ndarray:

@@ -375,6 +375,111 @@ int oracle_cluster_streaming(const ohit* h, uint64_t n, uint64_t dt, uint32_t W,
   return O_OK;
 }
 
+/* ------------------------------------------------ cluster shape records */
+/* Per cluster, in the order of feats[] (ascending label): the bounding box
+ * "smallest rectangle (aligned with the sensor) enclosing the cluster"
+ * (§3.3) and the unweighted second moments sum x^2, sum x*y,
+ * sum y^2 (shape features, §1 line 15; reading R19).  Plain
+ * definition: one pass over the hits, each hit added to the record of its
+ * label (label -> record position by a direct map). */
+typedef struct oshape {     /* 32-byte shape record */
+  uint16_t x_min, x_max, y_min, y_max;
+  uint64_t sum_xx, sum_xy, sum_yy;
+} oshape;
+
+int oracle_shapes(const ohit* h, uint64_t n, const uint32_t* labels, const ofeat* feats, uint64_t k,
+                  oshape* out) {
+  if (n && (!h || !labels || !feats || !out)) return O_ERR_ARG;
+  uint32_t* pos = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  if (!pos) return O_ERR_OOM;
+  for (uint64_t i = 0; i < n; ++i) pos[i] = UINT32_MAX;
+  for (uint64_t c = 0; c < k; ++c) {
+    pos[feats[c].label] = (uint32_t)c;
+    out[c].x_min = out[c].y_min = UINT16_MAX;
+    out[c].x_max = out[c].y_max = 0;
+    out[c].sum_xx = out[c].sum_xy = out[c].sum_yy = 0;
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t c = pos[labels[i]];
+    if (c == UINT32_MAX) { free(pos); return O_ERR_ARG; }
+    uint64_t x = h[i].x, y = h[i].y;
+    if (h[i].x < out[c].x_min) out[c].x_min = h[i].x;
+    if (h[i].x > out[c].x_max) out[c].x_max = h[i].x;
+    if (h[i].y < out[c].y_min) out[c].y_min = h[i].y;
+    if (h[i].y > out[c].y_max) out[c].y_max = h[i].y;
+    out[c].sum_xx += x * x;
+    out[c].sum_xy += x * y;
+    out[c].sum_yy += y * y;
+  }
+  free(pos);
+  return O_OK;
+}
+
+/* --------------------------------------------- cluster-contiguous output */
+/* Alg. "High-level GPU clustering" Step 6 (§4): "Sort
+ * clusters by their minimum time of arrival, causing the hits from the same
+ * cluster to form adjacent memory blocks".  Reading R18: hits are ordered by
+ * (toa, input index); a cluster's position is that of its earliest hit in
+ * this order (ties in minimum ToA broken by that hit's input index); inside a
+ * block, hits keep the (toa, input index) order.
+ *   order[n]       input indices, cluster blocks one after another
+ *   offsets[k+1]   block g is order[offsets[g] .. offsets[g+1])
+ *   cluster_of[k]  block g holds the cluster feats[cluster_of[g]]            */
+static _Thread_local const uint64_t* g_sort_keys;
+static int cmp_key_u32(const void* a, const void* b) {
+  uint32_t i = *(const uint32_t*)a, j = *(const uint32_t*)b;
+  uint64_t ki = g_sort_keys[i], kj = g_sort_keys[j];
+  if (ki != kj) return ki < kj ? -1 : 1;
+  return (i > j) - (i < j);
+}
+
+int oracle_group(const ohit* h, uint64_t n, const uint32_t* labels, const ofeat* feats, uint64_t k,
+                 uint32_t* order, uint64_t* offsets, uint32_t* cluster_of) {
+  if ((n && (!h || !labels || !feats || !order)) || !offsets || (k && !cluster_of)) return O_ERR_ARG;
+  uint32_t* S = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t* pos = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint64_t* first = (uint64_t*)malloc((k ? k : 1) * sizeof(uint64_t));
+  uint32_t* cl = (uint32_t*)malloc((k ? k : 1) * sizeof(uint32_t));
+  uint64_t* cursor = (uint64_t*)malloc((k ? k : 1) * sizeof(uint64_t));
+  uint32_t* block_of = (uint32_t*)malloc((k ? k : 1) * sizeof(uint32_t));
+  if (!S || !pos || !first || !cl || !cursor || !block_of) {
+    free(S); free(pos); free(first); free(cl); free(cursor); free(block_of);
+    return O_ERR_OOM;
+  }
+  /* 1. the (toa, input index) order of all hits */
+  for (uint64_t i = 0; i < n; ++i) S[i] = (uint32_t)i;
+  g_sort_hits = h;
+  qsort(S, n, sizeof(uint32_t), cmp_toa_id);
+  /* 2. label -> record position; each cluster's earliest position in S */
+  for (uint64_t i = 0; i < n; ++i) pos[i] = UINT32_MAX;
+  for (uint64_t c = 0; c < k; ++c) { pos[feats[c].label] = (uint32_t)c; first[c] = UINT64_MAX; }
+  for (uint64_t p = 0; p < n; ++p) {
+    uint32_t c = pos[labels[S[p]]];
+    if (c == UINT32_MAX) { n = 0; k = 0; break; }
+    if (first[c] == UINT64_MAX) first[c] = p;
+  }
+  /* 3. clusters in the order of their earliest hit */
+  for (uint64_t c = 0; c < k; ++c) cl[c] = (uint32_t)c;
+  g_sort_keys = first;
+  qsort(cl, k, sizeof(uint32_t), cmp_key_u32);
+  /* 4. block offsets from the cluster sizes */
+  offsets[0] = 0;
+  for (uint64_t g = 0; g < k; ++g) {
+    cluster_of[g] = cl[g];
+    block_of[cl[g]] = (uint32_t)g;
+    offsets[g + 1] = offsets[g] + feats[cl[g]].size;
+  }
+  /* 5. hits in S order appended to their cluster's block */
+  for (uint64_t g = 0; g < k; ++g) cursor[g] = offsets[g];
+  for (uint64_t p = 0; p < n; ++p) {
+    uint32_t g = block_of[pos[labels[S[p]]]];
+    order[cursor[g]++] = S[p];
+  }
+  int rc = (k && offsets[k] != n) ? O_ERR_ARG : O_OK;
+  free(S); free(pos); free(first); free(cl); free(cursor); free(block_of);
+  return rc;
+}
+
 /* ------------------------------------------------------------ centroid */
 /* cx = sum_tot_x / tot_sum, cy = sum_tot_y / tot_sum (one IEEE division each);
  * tot_sum == 0 -> unweighted sum_x / size (reading R8). */

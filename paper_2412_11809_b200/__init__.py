@@ -193,8 +193,9 @@ class Clusterer:
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
         return self._ws
 
-    def set_profiling(self, on: bool = True):
-        _set_profiling(self._h, 1 if on else 0)
+    def set_profiling(self, on: bool | int = True):
+        """False/0 off, True/1 stage events, 2 stage events + tile phase clocks."""
+        _check(_set_profiling(self._h, int(on)), "tpx_cluster_set_profiling")
 
     def set_tile_mode(self, mode: str = "auto"):
         """'auto' (density probe), 'sparse' or 'dense' tile configuration."""

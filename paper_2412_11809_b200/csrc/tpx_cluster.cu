@@ -286,7 +286,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.overflow = overflow;
   a.hdr = hdr;
   a.verify_stride = kWSortTile;
-  a.phase_cycles = c->profiling ? hdr->phase_cycles : nullptr;
+  a.phase_cycles = c->profiling >= 2 ? hdr->phase_cycles : nullptr;
   if (r.dense)
     k_tile_cc<tile_dense><<<L.tiles, kTileThreads, tile_smem_bytes<tile_dense>(), r.s>>>(a);
   else
@@ -417,7 +417,8 @@ int tpx_cluster_workspace_bytes(const tpx_cluster* c, uint64_t n, size_t* bytes)
 
 int tpx_cluster_set_profiling(tpx_cluster* c, int enable) {
   if (!c) return TPX_ERR_INVALID_ARG;
-  c->profiling = enable ? 1 : 0;
+  if (enable < 0 || enable > 2) return TPX_ERR_INVALID_ARG;
+  c->profiling = enable;
   return TPX_OK;
 }
 

@@ -249,3 +249,75 @@ def test_errors_and_empty():
     h = tpxgen.make_hits([(0, 512, 0)])
     with pytest.raises(oracle.OracleError):
         oracle.cluster(h, 10, 448, 512)
+
+
+# ------------------------------------------------ shapes and grouping (§8(f) f3)
+def _brute_shapes_and_groups(h, labels):
+    """Python loops over explicit member lists: bounding box,
+    second moments (reading R19), and the Step-6 block order (l.175, R18)."""
+    members = {}
+    for i, l in enumerate(labels.tolist()):
+        members.setdefault(l, []).append(i)
+    shapes = {}
+    for l, mem in members.items():
+        xs = [int(h["x"][i]) for i in mem]
+        ys = [int(h["y"][i]) for i in mem]
+        shapes[l] = (min(xs), max(xs), min(ys), max(ys), sum(x * x for x in xs),
+                     sum(x * y for x, y in zip(xs, ys)), sum(y * y for y in ys))
+    blocks = [sorted(mem, key=lambda i: (int(h["toa"][i]), i)) for mem in members.values()]
+    blocks.sort(key=lambda b: (int(h["toa"][b[0]]), b[0]))
+    return shapes, blocks
+
+
+def _check_shapes_group(h, dt, W=256, H=256):
+    labels, feats = oracle.cluster(h, dt, W, H)
+    sh = oracle.shapes(h, labels, feats)
+    order, offsets, cof = oracle.group(h, labels, feats)
+    bs, blocks = _brute_shapes_and_groups(h, labels)
+    assert len(sh) == len(feats) == len(bs)
+    for c in range(len(feats)):
+        assert tuple(int(v) for v in sh[c]) == bs[int(feats["label"][c])]
+    assert len(cof) == len(blocks)
+    assert int(offsets[0]) == 0 and int(offsets[-1]) == len(h)
+    for g, b in enumerate(blocks):
+        got = order[int(offsets[g]):int(offsets[g + 1])].tolist()
+        assert got == b, (g, got, b)
+        assert int(feats["label"][cof[g]]) == min(b)
+        assert int(feats["size"][cof[g]]) == len(b)
+
+
+def test_shapes_group_hand_examples():
+    # Step-6 order by minimum ToA: label 1's cluster (min ToA 10) precedes label 0's
+    h = tpxgen.make_hits([(5, 5, 100, 1), (50, 50, 10, 1), (5, 6, 105, 1), (51, 50, 10, 1)])
+    labels, feats = oracle.cluster(h, 10)
+    order, offsets, cof = oracle.group(h, labels, feats)
+    assert order.tolist() == [1, 3, 0, 2] and offsets.tolist() == [0, 2, 4] and cof.tolist() == [1, 0]
+    # equal minimum ToA: the earliest hit's input index decides (R18): (10, #1) < (10, #2)
+    h = tpxgen.make_hits([(5, 5, 20, 1), (50, 50, 10, 1), (6, 5, 10, 1)])
+    labels, feats = oracle.cluster(h, 10)
+    order, offsets, cof = oracle.group(h, labels, feats)
+    assert order.tolist() == [1, 2, 0] and offsets.tolist() == [0, 1, 3] and cof.tolist() == [1, 0]
+    # L-shaped cluster: bbox (1..2, 1..2), sum x^2 = 1+4+4, sum xy = 1+2+4, sum y^2 = 1+1+4
+    h = tpxgen.make_hits([(1, 1, 0, 3), (2, 1, 1, 3), (2, 2, 2, 3)])
+    labels, feats = oracle.cluster(h, 10)
+    sh = oracle.shapes(h, labels, feats)
+    assert tuple(int(v) for v in sh[0]) == (1, 2, 1, 2, 9, 7, 6)
+
+
+def test_shapes_group_vs_brute_fuzz():
+    rng = np.random.default_rng(99)
+    for _ in range(60):
+        W, H = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        dt = int(rng.choice([0, 2, 16]))
+        h = tpxgen.random_small(rng, int(rng.integers(1, 400)), W, H, max(4 * dt, 3))
+        _check_shapes_group(h, dt, W, H)
+    _check_shapes_group(tpxgen.generate("tiny"), 128)
+    _check_shapes_group(tpxgen.generate("heavyion", n_hits=20_000), 64)
+
+
+def test_group_empty():
+    h = np.zeros(0, dtype=tpxgen.HIT_DTYPE)
+    labels, feats = oracle.cluster(h, 10)
+    order, offsets, cof = oracle.group(h, labels, feats)
+    assert len(order) == 0 and offsets.tolist() == [0] and len(cof) == 0
+    assert len(oracle.shapes(h, labels, feats)) == 0

@@ -13,7 +13,7 @@ d = torch.from_numpy(h.view(np.uint8)).cuda()
 c = tpx.Clusterer(p["dt_max"], W, H)
 for _ in range(2):
     c.run(d)
-c.set_profiling(True)
+c.set_profiling(2)
 c.run(d)
 st = c.stats()
 names = ["meta", "stage+bucket", "scatter+rank", "search+union", "flatten", "sizes+pairs", "compact", "features", "outputs"]
