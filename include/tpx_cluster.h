@@ -141,6 +141,42 @@ int tpx_cluster_run_partial(tpx_cluster* ctx, const tpx_hit* hits, uint64_t n,
                             void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* Per-cluster shape record, 32 bytes: the bounding box, "the smallest
+ * rectangle (aligned with the sensor) enclosing the cluster" (§3.3
+ * l.132), and the unweighted second moments sum x^2, sum x*y, sum y^2 (shape
+ * features, §1 l.15; reading R19).  Coordinates are pixel indices. */
+typedef struct tpx_cluster_shape {
+  uint16_t x_min, x_max, y_min, y_max;
+  uint64_t sum_xx;
+  uint64_t sum_xy;
+  uint64_t sum_yy;
+} tpx_cluster_shape;
+
+/* tpx_cluster_run plus the cluster-contiguous hit order of Alg. "High-level
+ * GPU clustering" Step 6 (§4 l.175: "Sort clusters by their minimum
+ * time of arrival, causing the hits from the same cluster to form adjacent
+ * memory blocks"; reading R18: hits are ordered by (toa, input
+ * index), a cluster is placed by its earliest hit in that order, and inside
+ * its block the hits keep that order).  Uses tpx_cluster_workspace_bytes(n).
+ *   labels_out, features_out, capacity, n_clusters_out: as tpx_cluster_run;
+ *                  capacity must be >= n_clusters (else TPX_ERR_CAPACITY with
+ *                  valid labels and no grouping outputs).
+ *   shapes_out     DEVICE, `capacity` records in features_out order, or NULL.
+ *   order_out      DEVICE, n u32 input indices: block g is
+ *                  order_out[offsets_out[g] .. offsets_out[g+1]).
+ *   offsets_out    DEVICE, n_clusters + 1 u32 (offsets_out[n_clusters] = n).
+ *   cluster_of_out DEVICE, n_clusters u32: block g holds the cluster
+ *                  features_out[cluster_of_out[g]].
+ * Returns after the whole pass completed on `stream` (stream sync). */
+int tpx_cluster_run_grouped(tpx_cluster* ctx, const tpx_hit* hits, uint64_t n,
+                            uint32_t* labels_out,
+                            tpx_cluster_features* features_out,
+                            tpx_cluster_shape* shapes_out, uint64_t capacity,
+                            uint64_t* n_clusters_out, uint32_t* order_out,
+                            uint32_t* offsets_out, uint32_t* cluster_of_out,
+                            void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* Device workspace needed by tpx_cluster_run_host: device staging for the
  * hits, labels and `capacity` feature records plus tpx_cluster_run's own. */
 int tpx_cluster_host_workspace_bytes(const tpx_cluster* ctx, uint64_t n,

@@ -75,6 +75,8 @@ _stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
 _run_partial = _proto("tpx_cluster_run_partial", _int, _vp, _vp, _u64, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
                       _vp, ctypes.c_size_t, _vp)
 _size_t_p = ctypes.POINTER(ctypes.c_size_t)
+_run_grouped = _proto("tpx_cluster_run_grouped", _int, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64),
+                      _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp)
 # host-buffer pipeline (include/tpx_cluster.h, "Host-buffer pipeline")
 _pipe_ws = _proto("tpx_pipeline_workspace_bytes", _int, _vp, _u64, _u64, _int, _size_t_p)
 _pipe_create = _proto("tpx_pipeline_create", _int, _u64, _int, _u32, _u32, _u64, _u64, _int, _vp, ctypes.c_size_t,
@@ -235,6 +237,36 @@ class Clusterer:
         kk = min(k.value, capacity)
         return labels[:n], features[:kk], k.value
 
+    def run_grouped(self, hits, n: int | None = None, shapes: bool = True, stream=None):
+        """``tpx_cluster_run_grouped``: labels, features, optional shape records
+        and the cluster-contiguous order (Alg. GPU Step 6).
+
+        Returns ``(labels, features, shapes|None, order, offsets, cluster_of, k)``
+        (device tensors; offsets has k + 1 entries).
+        """
+        torch = _torch()
+        assert hits.is_cuda and hits.is_contiguous()
+        if n is None:
+            n = hits.numel() * hits.element_size() // 16
+        dev = hits.device
+        cap = max(n, 1)
+        labels = torch.empty(cap, dtype=torch.int32, device=dev)
+        features = torch.empty((cap, 64), dtype=torch.uint8, device=dev)
+        shp = torch.empty((cap, 32), dtype=torch.uint8, device=dev) if shapes else None
+        order = torch.empty(cap, dtype=torch.int32, device=dev)
+        offsets = torch.empty(cap + 1, dtype=torch.int32, device=dev)
+        cluster_of = torch.empty(cap, dtype=torch.int32, device=dev)
+        workspace = self._workspace(self.workspace_bytes(n), dev)
+        k = _u64(0)
+        rc = _run_grouped(self._h, hits.data_ptr(), int(n), labels.data_ptr(), features.data_ptr(),
+                          shp.data_ptr() if shapes else None, int(cap), ctypes.byref(k), order.data_ptr(),
+                          offsets.data_ptr(), cluster_of.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                          _stream_handle(stream))
+        _check(rc, "tpx_cluster_run_grouped")
+        kk = k.value
+        return (labels[:n], features[:kk], shp[:kk] if shapes else None, order[:n], offsets[: kk + 1],
+                cluster_of[:kk], kk)
+
     def run_partial(self, hits, n: int, n_owned: int, stream=None):
         """``tpx_cluster_run_partial``: the first n_owned hits are owned, the rest
         a borrowed halo (features and records only from owned hits)."""
@@ -352,6 +384,18 @@ def centroids(features, stream=None):
     if rc != TPX_OK:
         raise TpxError(rc, "tpx_cluster_centroids")
     return out[:k]
+
+
+SHAPE_DTYPE = np.dtype(
+    [("x_min", "<u2"), ("x_max", "<u2"), ("y_min", "<u2"), ("y_max", "<u2"),
+     ("sum_xx", "<u8"), ("sum_xy", "<u8"), ("sum_yy", "<u8")]
+)
+
+
+def shapes_to_numpy(t) -> np.ndarray:
+    """A (k, 32) uint8 tensor of tpx_cluster_shape records -> structured array."""
+    a = t.contiguous().cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+    return a.reshape(-1).view(SHAPE_DTYPE).copy()
 
 
 def features_to_numpy(features) -> np.ndarray:

@@ -277,7 +277,6 @@ struct feat_acc {
 template <class C>
 __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args a) {
   using SL = tile_smem_layout<C>;
-  constexpr int kFwdMax = C::kFwdMax;
   constexpr int kStageItems = C::kStageItems;
   extern __shared__ __align__(16) unsigned char sm[];
   uint2* csort = reinterpret_cast<uint2*>(sm + SL::csort);      // (toa - base, y<<16|x), bucket-sorted

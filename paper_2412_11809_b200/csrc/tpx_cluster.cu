@@ -18,6 +18,7 @@
 #include "cluster.cuh"
 #include "common.cuh"
 #include "finalize.cuh"
+#include "group.cuh"
 #include "scan.cuh"
 #include "shard.cuh"
 #include "sort.cuh"
@@ -36,7 +37,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 uint32_t n_tiles_of(uint64_t n, int tile) { return (uint32_t)((n + tile - 1) / tile); }
 
 struct layout {
-  size_t hdr, S, parent, slot_of, stage, comp_count, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
+  size_t hdr, probe, S, parent, slot_of, stage, comp_count, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
   size_t keys0, keys1, vals0, vals1, hist, minidx, flags, ord;
   size_t total;
   uint32_t tiles, nwords;
@@ -56,6 +57,7 @@ layout make_layout(uint64_t n) {
   uint32_t st = n_tiles_of((uint64_t)rt * kRadixBins, kScanTile);
   st = st > n_tiles_of(n, kScanTile) ? st : n_tiles_of(n, kScanTile);
   L.hdr = take(sizeof(dev_hdr));
+  L.probe = take(kProbeSamples * 4);
   L.S = take(n * 16);
   L.parent = take(n * 4);
   L.slot_of = take(n * 4);
@@ -489,21 +491,29 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       if ((rc = sort_global(c, r))) return rc;
     }
     c->stats.sort_path = attempt >= 2 ? 1 : 0;
-    // window-density probe (one small read-back): dense heavy-ion windows use
-    // the large-halo tile configuration
-    if (c->tile_mode != TPX_TILE_AUTO) {
-      r.dense = c->tile_mode == TPX_TILE_DENSE;
-      c->stats.tile_dense = r.dense ? 1 : 0;
-    } else {
-      uint32_t* probe = (uint32_t*)(r.ws + r.L.wcnt);  // scratch: wcnt is rewritten by k_popc later
-      k_density_probe<<<1, kProbeSamples, 0, r.s>>>(S, n, c->dt, probe);
-      TPX_LAUNCHED(c);
+    // one small read-back after the sort: validation and window-sort status
+    // (a window wider than 32 bits of ticks leaves its output tile unwritten,
+    // so the tile kernel must not run on it) and the window-density probe
+    // (dense heavy-ion windows use the large-halo tile configuration)
+    {
+      const bool probe_on = c->tile_mode == TPX_TILE_AUTO;
+      uint32_t* probe = (uint32_t*)(r.ws + r.L.probe);
       uint32_t hprobe[kProbeSamples];
-      TPX_CUDA(cudaMemcpyAsync(hprobe, probe, sizeof(hprobe), cudaMemcpyDeviceToHost, r.s));
-      TPX_CUDA(cudaStreamSynchronize(r.s));
-      int big = 0;
-      for (int i = 0; i < kProbeSamples; ++i) big += hprobe[i] > (uint32_t)(tile_sparse::kHalo * 5 / 8);
-      r.dense = big * 10 > kProbeSamples;  // > 10 % of the samples have windows near the sparse halo
+      if (probe_on) {
+        k_density_probe<<<1, kProbeSamples, 0, r.s>>>(S, n, c->dt, probe);
+        TPX_LAUNCHED(c);
+        TPX_CUDA(cudaMemcpyAsync(hprobe, probe, sizeof(hprobe), cudaMemcpyDeviceToHost, r.s));
+      }
+      if ((rc = read_header(c, r))) return rc;
+      if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
+      if (attempt < 2 && c->host_hdr->sort_bad) continue;
+      if (probe_on) {
+        int big = 0;
+        for (int i = 0; i < kProbeSamples; ++i) big += hprobe[i] > (uint32_t)(tile_sparse::kHalo * 5 / 8);
+        r.dense = big * 10 > kProbeSamples;  // > 10 % of the samples have windows near the sparse halo
+      } else {
+        r.dense = c->tile_mode == TPX_TILE_DENSE;
+      }
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
     c->stats.sort_retries = attempt < 2 ? attempt : 2;
@@ -538,6 +548,103 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     }
   }
   return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
+}
+
+int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* labels_out,
+                            tpx_cluster_features* features_out, tpx_cluster_shape* shapes_out, uint64_t capacity,
+                            uint64_t* n_clusters_out, uint32_t* order_out, uint32_t* offsets_out,
+                            uint32_t* cluster_of_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!c || !n_clusters_out) return TPX_ERR_INVALID_ARG;
+  *n_clusters_out = 0;
+  if (n && (!order_out || !offsets_out || !cluster_of_out || !features_out || capacity == 0)) return TPX_ERR_INVALID_ARG;
+  if (((uintptr_t)order_out & 3) || ((uintptr_t)offsets_out & 3) || ((uintptr_t)cluster_of_out & 3) ||
+      ((uintptr_t)shapes_out & 15))
+    return TPX_ERR_INVALID_ARG;
+  uint64_t k = 0;
+  int rc = tpx_cluster_run_partial(c, hits, n, n, labels_out, features_out, capacity, &k, workspace,
+                                   workspace_bytes, stream);
+  *n_clusters_out = k;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (rc == TPX_OK && n == 0 && offsets_out) {
+    TPX_CUDA(cudaMemsetAsync(offsets_out, 0, 4, s));
+    TPX_CUDA(cudaStreamSynchronize(s));
+  }
+  if (rc != TPX_OK || n == 0) return rc;
+  const layout L = make_layout(n);
+  char* ws = (char*)workspace;
+  // after the run only S (sorted records) is live; the scratch regions are reused
+  const srec* S = (const srec*)(ws + L.S);
+  uint32_t* rbits = (uint32_t*)(ws + L.bitmap);
+  uint32_t* rbase = (uint32_t*)(ws + L.wcnt);
+  uint32_t* fbits = (uint32_t*)(ws + L.open_hits);
+  uint32_t* fbase = (uint32_t*)(ws + L.open_comps);
+  uint32_t* cpos = (uint32_t*)(ws + L.minidx);
+  uint32_t* first = (uint32_t*)(ws + L.flags);
+  uint32_t* grank = (uint32_t*)(ws + L.ord);
+  uint32_t* gsize = (uint32_t*)(ws + L.parent);
+  uint32_t* k0 = (uint32_t*)(ws + L.keys0);
+  uint32_t* k1 = (uint32_t*)(ws + L.keys1);
+  uint32_t* v0 = (uint32_t*)(ws + L.vals0);
+  uint32_t* v1 = (uint32_t*)(ws + L.vals1);
+  uint32_t* hist = (uint32_t*)(ws + L.hist);
+  uint32_t* partials = (uint32_t*)(ws + L.partials);
+  const uint64_t nwords = L.nwords;
+  const int gn = grid_for(n, 256), gk = grid_for(k, 256), gw = grid_for(nwords, 256);
+  // G0: label -> ordinal
+  k_root_bits<<<gw, 256, 0, s>>>(labels_out, n, rbits);
+  TPX_LAUNCHED(c);
+  k_popc<<<gw, 256, 0, s>>>(rbits, nwords, rbase);
+  TPX_LAUNCHED(c);
+  if ((rc = exclusive_scan(c, rbase, nwords, rbase, partials, nullptr, s))) return rc;
+  // G1: first sorted position per cluster
+  TPX_CUDA(cudaMemsetAsync(first, 0xff, k * 4, s));
+  k_group_first<<<gn, 256, 0, s>>>(S, n, labels_out, rbits, rbase, cpos, first);
+  TPX_LAUNCHED(c);
+  // G2/G3: block index of each cluster, block table, offsets
+  TPX_CUDA(cudaMemsetAsync(fbits, 0, nwords * 4, s));
+  k_mark_first<<<gk, 256, 0, s>>>(first, k, fbits);
+  TPX_LAUNCHED(c);
+  k_popc<<<gw, 256, 0, s>>>(fbits, nwords, fbase);
+  TPX_LAUNCHED(c);
+  if ((rc = exclusive_scan(c, fbase, nwords, fbase, partials, nullptr, s))) return rc;
+  k_group_rank<<<gk, 256, 0, s>>>(first, k, fbits, fbase, features_out, grank, cluster_of_out, gsize);
+  TPX_LAUNCHED(c);
+  if ((rc = exclusive_scan(c, gsize, k, offsets_out, partials, offsets_out + k, s))) return rc;
+  // G4: stable radix sort of (block index, input index) in S order
+  k_group_keys<<<gn, 256, 0, s>>>(S, n, cpos, grank, k0, v0);
+  TPX_LAUNCHED(c);
+  const int bits = k > 1 ? 64 - __builtin_clzll(k - 1) : 0;
+  const int passes = bits ? (bits + 7) / 8 : 0;
+  const uint32_t tiles = n_tiles_of(n, kRadixTile);
+  if (passes == 0) {
+    TPX_CUDA(cudaMemcpyAsync(order_out, v0, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    const bool last = p == passes - 1;
+    uint32_t* vout = last ? order_out : v1;
+    k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, shift, hist, tiles);
+    TPX_LAUNCHED(c);
+    if ((rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s))) return rc;
+    k_radix_scatter<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, shift, hist, tiles, k1,
+                                                                      vout);
+    TPX_LAUNCHED(c);
+    uint32_t* t = k0;
+    k0 = k1;
+    k1 = t;
+    t = v0;
+    v0 = v1;
+    v1 = t;
+  }
+  // G5: shape records
+  if (shapes_out) {
+    k_shapes_small<<<gk, 256, 0, s>>>(hits, order_out, offsets_out, cluster_of_out, k, (shape_rec*)shapes_out);
+    TPX_LAUNCHED(c);
+    k_shapes_large<<<gk, 256, 0, s>>>(hits, order_out, offsets_out, cluster_of_out, k, (shape_rec*)shapes_out);
+    TPX_LAUNCHED(c);
+  }
+  TPX_CUDA(cudaStreamSynchronize(s));
+  return TPX_OK;
 }
 
 int tpx_cluster_host_workspace_bytes(const tpx_cluster* c, uint64_t n, uint64_t capacity, size_t* bytes) {
