@@ -143,28 +143,34 @@ __global__ void k_popc(const uint32_t* __restrict__ bitmap, uint64_t nwords, uin
 }
 
 // A6 + A7: ordinal of a label = set bits below it in the label bitmap; copy
-// the staged record to features_out[ordinal] (ascending label order).
-__global__ void __launch_bounds__(256) k_emit(const tpx_cluster_features* __restrict__ stage,
-                                              const uint32_t* __restrict__ comp_count,
-                                              const uint32_t* __restrict__ bitmap,
-                                              const uint32_t* __restrict__ wbase,
-                                              tpx_cluster_features* __restrict__ out, uint64_t capacity) {
-  const uint32_t cc = comp_count[blockIdx.x];
-  const uint64_t t0 = (uint64_t)blockIdx.x * kTile;
-  for (uint32_t c = threadIdx.x; c < cc; c += blockDim.x) {
-    const uint4* src = reinterpret_cast<const uint4*>(stage + t0 + c);
-    const uint4 q0 = __ldcs(src);
-    const uint32_t size = q0.y;
-    if (size == 0) continue;
-    const uint32_t label = q0.x;
-    const uint32_t w = label >> 5;
-    const uint64_t ord = (uint64_t)wbase[w] + __popc(bitmap[w] & ((1u << (label & 31)) - 1u));
-    if (ord >= capacity) continue;
-    uint4* dst = reinterpret_cast<uint4*>(out + ord);
-    dst[0] = q0;
-    dst[1] = __ldcs(src + 1);
-    dst[2] = __ldcs(src + 2);
-    dst[3] = __ldcs(src + 3);
+// the staged record to features_out[ordinal] (ascending label order).  One
+// warp per tile (persistent grid): the tile's records are read as a flat run
+// of 16-byte words, so every load instruction covers 512 contiguous bytes.
+constexpr int kEmitThreads = 256;
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_features* __restrict__ stage,
+                                                       const uint32_t* __restrict__ comp_count, uint32_t n_tiles,
+                                                       const uint32_t* __restrict__ bitmap,
+                                                       const uint32_t* __restrict__ wbase,
+                                                       tpx_cluster_features* __restrict__ out, uint64_t capacity) {
+  const unsigned lane = lane_id();
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
+    const uint32_t cc = comp_count[t];
+    const uint4* src = reinterpret_cast<const uint4*>(stage + (uint64_t)t * kTile);
+    for (uint32_t q0 = 0; q0 < cc * 4; q0 += 32) {  // warp-uniform trip count
+      const uint32_t q = q0 + lane;
+      const bool valid = q < cc * 4;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (valid) v = __ldcs(src + q);
+      // the record's first word (label, size) sits in the group's first lane
+      const uint32_t label = __shfl_sync(kFull, v.x, lane & ~3u);
+      const uint32_t size = __shfl_sync(kFull, v.y, lane & ~3u);
+      if (!valid || size == 0) continue;
+      const uint32_t w = label >> 5;
+      const uint64_t ord = (uint64_t)wbase[w] + __popc(bitmap[w] & ((1u << (label & 31)) - 1u));
+      if (ord >= capacity) continue;
+      reinterpret_cast<uint4*>(out + ord)[q & 3] = v;
+    }
   }
 }
 

@@ -314,7 +314,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   int rc = exclusive_scan(c, wcnt, L.nwords, wcnt, partials, (uint32_t*)&hdr->n_clusters, r.s);
   if (rc) return rc;
   if (r.capacity) {
-    k_emit<<<L.tiles, 256, 0, r.s>>>(stage, comp_count, bitmap, wcnt, r.feats, r.capacity);
+    k_emit<<<kListGrid, kEmitThreads, 0, r.s>>>(stage, comp_count, L.tiles, bitmap, wcnt, r.feats, r.capacity);
     TPX_LAUNCHED(c);
   }
   if (c->profiling) cudaEventRecord(c->ev[4], r.s);
