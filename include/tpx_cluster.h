@@ -383,6 +383,95 @@ int tpx_shard_fold_features(const tpx_cluster_features* kept, uint64_t n_kept,
                             void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* ------------------------------------------------------------------------
+ * Streaming ingest: Alg. "Hit buffer filling" (PAPER.md
+ * §4 l.184-213) feeding Alg. "High-level GPU clustering" (l.160-182) with
+ * exact carry-over of clusters open at a buffer border.
+ *
+ * Hits are pushed in readout (arrival) order; arrival index a = number of
+ * hits pushed before.  A buffer is sent when storeHit says so; its cut is
+ * C = toa_max + t_closing, and since the stream is t-ordered (l.99-100) every
+ * later hit has toa >= C.  A cluster with a hit within dt_max of C stays open:
+ * its hits are kept on the device and clustered again with the next buffer;
+ * every other cluster is final and is emitted in a batch.  The union of all
+ * batches equals tpx_cluster_run on the whole stream, with
+ *   label = the smallest ARRIVAL index of the cluster (u64),
+ * and in each batch clusters in Step-6 order (l.175, reading R18: by earliest
+ * hit in (toa, arrival index) order), each cluster's hits contiguous in
+ * (toa, arrival index) order (Step 8: "Transfer hits and labels").  Hits that
+ * violate t-orderedness (toa < the last sent cut) are counted in late_hits;
+ * results are then not guaranteed exact.  Device memory: caller workspace.
+ * Not thread-safe.  Buffers are clustered synchronously inside push/flush on
+ * `cuda_stream`.
+ */
+typedef struct tpx_stream tpx_stream;
+
+typedef struct tpx_stream_config {
+  uint64_t dt_max_ticks;     /* Delta t_max (ToA ticks)                       */
+  uint32_t width, height;    /* sensor size, as tpx_cluster_create            */
+  uint64_t buffer_hits;      /* b: maximum buffer size                        */
+  uint64_t reserve_hits;     /* b_t < b: hits that can arrive in t + t_closing */
+  uint64_t disorder_ticks;   /* t: the stream is t-ordered                    */
+  uint64_t closing_ticks;    /* t_closing (expected cluster duration)         */
+  uint64_t max_device_hits;  /* >= b + b_t: device room per buffer including
+                                the carried hits of open clusters (< 2^32-1) */
+} tpx_stream_config;
+
+/* One emitted cluster, 80 bytes.  Hits: batch.hits[offset .. offset+size). */
+typedef struct tpx_stream_cluster {
+  uint64_t label;            /* smallest arrival index in the cluster         */
+  uint64_t offset;           /* first hit of the cluster in the batch         */
+  uint32_t size;
+  uint32_t reserved;
+  uint64_t toa_min, toa_max, tot_sum, sum_x, sum_y, sum_tot_x, sum_tot_y;
+} tpx_stream_cluster;
+
+typedef struct tpx_stream_batch {
+  uint64_t seq;                        /* buffer sequence number             */
+  uint64_t n_clusters, n_hits;
+  const tpx_stream_cluster* clusters;  /* HOST, owned by the stream, valid
+                                          until the next pop or destroy      */
+  const tpx_hit* hits;                 /* HOST, n_hits, cluster blocks       */
+  const uint64_t* hit_index;           /* HOST, n_hits arrival indices       */
+} tpx_stream_batch;
+
+typedef struct tpx_stream_stats {
+  uint64_t hits_in, hits_out, clusters_out, buffers;
+  uint64_t carried_max, carried_last;  /* hits of open clusters kept on device */
+  uint64_t late_hits;                  /* t-orderedness violations           */
+  double device_ms;                    /* summed per-buffer H2D..D2H time    */
+} tpx_stream_stats;
+
+/* Errors: INVALID_ARG (b <= b_t, max_device_hits < b + b_t or >= 2^32-1). */
+int tpx_stream_workspace_bytes(const tpx_stream_config* cfg, size_t* bytes);
+/* workspace: DEVICE, 256-B aligned, >= tpx_stream_workspace_bytes.  *out is
+ * owned by the library (tpx_stream_destroy).  Errors: INVALID_ARG, OOM, CUDA. */
+int tpx_stream_create(const tpx_stream_config* cfg, void* workspace,
+                      size_t workspace_bytes, void* cuda_stream,
+                      tpx_stream** out);
+/* hits_host: HOST, n records in arrival order (copied; pinned not required).
+ * Clusters every buffer that becomes full.  Errors: INVALID_ARG (after
+ * flush), CAPACITY (a buffer plus carried hits exceeds max_device_hits), OOM,
+ * CUDA, COORD_RANGE. */
+int tpx_stream_push(tpx_stream* s, const tpx_hit* hits_host, uint64_t n);
+/* End of stream: sends what is buffered; every cluster is closed. */
+int tpx_stream_flush(tpx_stream* s);
+/* Returns 1 and fills *out with the oldest unread batch, 0 if none (<0 on
+ * error).  The previous batch's memory is recycled by this call. */
+int tpx_stream_pop(tpx_stream* s, tpx_stream_batch* out);
+int tpx_stream_get_stats(const tpx_stream* s, tpx_stream_stats* out);
+void tpx_stream_destroy(tpx_stream* s);
+
+/* Host-only helper (no GPU): the buffer each hit is sent in by Alg. "Hit
+ * buffer filling" (buffer_id_out[n], HOST) and each buffer's cut (cuts_out,
+ * HOST, cuts_cap entries; the final buffer's cut is UINT64_MAX), exactly as
+ * tpx_stream_push/flush assign them.  Errors: INVALID_ARG, CAPACITY
+ * (more than cuts_cap buffers; *n_buffers_out holds the count). */
+int tpx_buffill_assign(const tpx_hit* hits, uint64_t n, uint64_t b,
+                       uint64_t b_t, uint64_t t, uint64_t t_closing,
+                       uint32_t* buffer_id_out, uint64_t* cuts_out,
+                       uint64_t cuts_cap, uint64_t* n_buffers_out);
+
 #ifdef __cplusplus
 }
 #endif

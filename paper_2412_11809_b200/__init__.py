@@ -309,6 +309,119 @@ class Clusterer:
         return k.value
 
 
+class StreamConfig(ctypes.Structure):
+    _fields_ = [("dt_max_ticks", _u64), ("width", _u32), ("height", _u32), ("buffer_hits", _u64),
+                ("reserve_hits", _u64), ("disorder_ticks", _u64), ("closing_ticks", _u64),
+                ("max_device_hits", _u64)]
+
+
+class StreamBatch(ctypes.Structure):
+    _fields_ = [("seq", _u64), ("n_clusters", _u64), ("n_hits", _u64), ("clusters", _vp), ("hits", _vp),
+                ("hit_index", _vp)]
+
+
+class StreamStats(ctypes.Structure):
+    _fields_ = [("hits_in", _u64), ("hits_out", _u64), ("clusters_out", _u64), ("buffers", _u64),
+                ("carried_max", _u64), ("carried_last", _u64), ("late_hits", _u64), ("device_ms", ctypes.c_double)]
+
+
+#: 80-byte tpx_stream_cluster record.
+STREAM_CLUSTER_DTYPE = np.dtype(
+    [("label", "<u8"), ("offset", "<u8"), ("size", "<u4"), ("reserved", "<u4"), ("toa_min", "<u8"),
+     ("toa_max", "<u8"), ("tot_sum", "<u8"), ("sum_x", "<u8"), ("sum_y", "<u8"), ("sum_tot_x", "<u8"),
+     ("sum_tot_y", "<u8")]
+)
+assert STREAM_CLUSTER_DTYPE.itemsize == 80
+_HIT_DTYPE = np.dtype([("toa", "<u8"), ("x", "<u2"), ("y", "<u2"), ("tot", "<u2"), ("reserved", "<u2")])
+
+_stream_ws = _proto("tpx_stream_workspace_bytes", _int, ctypes.POINTER(StreamConfig), _size_t_p)
+_stream_create = _proto("tpx_stream_create", _int, ctypes.POINTER(StreamConfig), _vp, ctypes.c_size_t, _vp,
+                        ctypes.POINTER(_vp))
+_stream_push = _proto("tpx_stream_push", _int, _vp, _vp, _u64)
+_stream_flush = _proto("tpx_stream_flush", _int, _vp)
+_stream_pop = _proto("tpx_stream_pop", _int, _vp, ctypes.POINTER(StreamBatch))
+_stream_stats = _proto("tpx_stream_get_stats", _int, _vp, ctypes.POINTER(StreamStats))
+_stream_destroy = _proto("tpx_stream_destroy", None, _vp)
+_buffill_assign = _proto("tpx_buffill_assign", _int, _vp, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _u64,
+                         ctypes.POINTER(_u64))
+
+
+def buffill_assign(hits: np.ndarray, b: int, b_t: int, t: int, t_closing: int):
+    """Host-only: buffer id per hit and the cut of each buffer, as the stream
+    assigns them (Alg. "Hit buffer filling")."""
+    h = np.ascontiguousarray(hits)
+    n = len(h)
+    ids = np.zeros(max(n, 1), dtype=np.uint32)
+    cap = n + 2
+    cuts = np.zeros(cap, dtype=np.uint64)
+    nb = _u64(0)
+    _check(_buffill_assign(h.ctypes.data if n else None, n, int(b), int(b_t), int(t), int(t_closing),
+                           ids.ctypes.data, cuts.ctypes.data, cap, ctypes.byref(nb)), "tpx_buffill_assign")
+    return ids[:n], [int(c) for c in cuts[: nb.value]]
+
+
+class Stream:
+    """``tpx_stream_*``: push hits in readout order, pop batches of final
+    clusters (labels = smallest arrival index; Step-6 order)."""
+
+    def __init__(self, dt_max: int, buffer_hits: int, reserve_hits: int, disorder_ticks: int, closing_ticks: int,
+                 max_device_hits: int | None = None, width: int = 256, height: int = 256, stream=None):
+        torch = _torch()
+        cfg = StreamConfig(int(dt_max), int(width), int(height), int(buffer_hits), int(reserve_hits),
+                           int(disorder_ticks), int(closing_ticks),
+                           int(max_device_hits or 2 * (buffer_hits + reserve_hits)))
+        b = ctypes.c_size_t(0)
+        _check(_stream_ws(ctypes.byref(cfg), ctypes.byref(b)), "tpx_stream_workspace_bytes")
+        self._ws = torch.empty(max(b.value, 256), dtype=torch.uint8, device="cuda")
+        h = _vp()
+        _check(_stream_create(ctypes.byref(cfg), self._ws.data_ptr(), self._ws.numel(), _stream_handle(stream),
+                              ctypes.byref(h)), "tpx_stream_create")
+        self._h = h
+
+    def push(self, hits: np.ndarray):
+        h = np.ascontiguousarray(hits)
+        assert h.dtype.itemsize == 16
+        _check(_stream_push(self._h, h.ctypes.data if len(h) else None, len(h)), "tpx_stream_push")
+
+    def flush(self):
+        _check(_stream_flush(self._h), "tpx_stream_flush")
+
+    def pop(self):
+        """Next batch as numpy copies ``{seq, clusters, hits, hit_index}`` or None."""
+        bt = StreamBatch()
+        r = _stream_pop(self._h, ctypes.byref(bt))
+        if r < 0:
+            _check(r, "tpx_stream_pop")
+        if r == 0:
+            return None
+
+        def arr(ptr, n, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            buf = (ctypes.c_uint8 * (n * dt.itemsize)).from_address(ptr)
+            return np.frombuffer(buf, dtype=dt).copy()
+
+        return {"seq": bt.seq, "clusters": arr(bt.clusters, bt.n_clusters, STREAM_CLUSTER_DTYPE),
+                "hits": arr(bt.hits, bt.n_hits, _HIT_DTYPE), "hit_index": arr(bt.hit_index, bt.n_hits,
+                                                                             np.dtype("<u8"))}
+
+    def stats(self) -> dict:
+        st = StreamStats()
+        _check(_stream_stats(self._h, ctypes.byref(st)), "tpx_stream_get_stats")
+        return {k: getattr(st, k) for k, _ in StreamStats._fields_}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _stream_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Pipeline:
     """``tpx_pipeline_*``: overlap host<->device copies of one buffer with the
     kernels of another (``depth`` slots, native worker threads).  Buffers are

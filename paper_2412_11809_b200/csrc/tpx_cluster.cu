@@ -969,3 +969,5 @@ int tpx_shard_fold_features(const tpx_cluster_features* kept, uint64_t n_kept, c
 }
 
 }  // extern "C"
+
+#include "stream.cuh"
