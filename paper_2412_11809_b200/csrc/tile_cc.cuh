@@ -25,6 +25,8 @@
 //      64-byte record staged; open components stage a partial record that the
 //      global pass merges.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "sort.cuh"
 
@@ -33,8 +35,11 @@ namespace tpx {
 constexpr int kTileThreads = 256;
 constexpr int kTile = 1024;                    // tile hits per CTA
 constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
-constexpr int kBuckets = 1024;                 // one bucket per pixel column (wider sensors: global path)
-constexpr int kBucketCap = 512;                // longer buckets: the tile takes the global path
+constexpr uint32_t kPixEmpty = 0xfffffu;       // empty hash slot key (pixel ids must be < 2^20 - 1)
+constexpr uint32_t kMaxTilePixels = 0xfffffu;  // sensors with more pixels take the global path
+constexpr uint16_t kNil = 0xffffu;             // end of a pixel list
+constexpr int kBuckets = 1024;                 // sparse: one bucket per pixel column (wider sensors: global path)
+constexpr int kBucketCap = 512;                // sparse: longer buckets take the global path
 constexpr int kItemsPerThread = kTile / kTileThreads;      // 4
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and chunk
@@ -43,23 +48,29 @@ constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and 
 // the tile's last hit.  Sparse streams (windows of tens of hits) use a 1024
 // halo and fit 4 CTAs per SM; dense heavy-ion streams (windows of ~1-3k hits,
 // SURVEY H1) use a 3072 halo at 2 CTAs per SM so that windows stay on chip.
-template <int kHaloHits, int kMinBlocks>
+template <int kHaloHits, int kMinBlocks, bool kHashIndex>
 struct tile_cfg {
   static constexpr int kHalo = kHaloHits;
   static constexpr int kFwdMax = kTile + kHaloHits;               // tile + forward halo (local index l)
   static constexpr int kStageItems = kFwdMax / kTileThreads;
   static constexpr bool kRegStage = kStageItems <= 8;             // stage in registers, else re-read S
   static constexpr int kBlocks = kMinBlocks;
+  static constexpr bool kHash = kHashIndex;                       // pixel hash (dense) vs column buckets (sparse)
+  static constexpr int kSlotBits = kHaloHits > 1024 ? 13 : 12;   // pixel hash slots (load <= 1/2)
+  static constexpr int kSlots = 1 << kSlotBits;
   static_assert(kFwdMax % kTileThreads == 0, "staging layout");
+  static_assert(kFwdMax <= 4096, "12-bit list heads");
+  static_assert(kSlots >= 2 * kFwdMax, "hash load");
 };
-using tile_sparse = tile_cfg<1024, 4>;
-using tile_dense = tile_cfg<3072, 2>;
+using tile_sparse = tile_cfg<1024, 4, false>;
+using tile_dense = tile_cfg<3072, 2, true>;
 
 struct tile_args {
   const srec* S;
   uint64_t n;
   uint64_t dt;
   uint32_t width;
+  uint32_t height;
   uint32_t n_owned;          // hits with input index >= n_owned carry no features (sharded halo)
   uint32_t* labels;          // labels_out (input order)
   uint32_t* parent_g;        // global union-find over sorted positions (open hits only)
@@ -167,10 +178,10 @@ __device__ __forceinline__ void set_label_bit(uint32_t* bitmap, uint32_t label) 
   atomicOr(bitmap + (label >> 5), 1u << (label & 31));
 }
 
-// Shared-memory carve-up (bytes).  Region A holds the column index during the
-// clustering phase and the staged hits + member array + labels afterwards.
+// Shared-memory carve-up of the column-bucket index (sparse configuration),
+// bytes.  Region A holds the column index during the clustering phase and the staged hits + member array + labels afterwards.
 template <class C>
-struct tile_smem_layout {
+struct tile_smem_buckets {
   static constexpr size_t kFwdMax = C::kFwdMax;
   static constexpr size_t csort = 0;                                   // uint2 [kFwdMax] (toa - base, y<<16|x)
   static constexpr size_t ckey = csort + (size_t)kFwdMax * 8;           // u32   [kFwdMax] y<<16 | local index
@@ -198,6 +209,37 @@ struct tile_smem_layout {
   static constexpr size_t eslot = hflag + kTile;                       // u16   [kFwdMax] (dense staging)
   static constexpr size_t total = eslot + (C::kRegStage ? 0 : (size_t)kFwdMax * 2);
 };
+// Shared-memory carve-up of the pixel-hash index (dense configuration), bytes.
+// Region A holds the hash index during the clustering phase and the staged hits + member array + labels afterwards.
+template <class C>
+struct tile_smem_hash {
+  static constexpr size_t kFwdMax = C::kFwdMax;
+  static constexpr size_t tab = 0;                                      // u32 [kSlots] pixel << 12 | list head
+  static constexpr size_t stoa = tab + (size_t)C::kSlots * 4;           // u32 [kFwdMax] toa - base
+  static constexpr size_t nxt = stoa + (size_t)kFwdMax * 4;             // u16 [kFwdMax] next in pixel list
+  static constexpr size_t sxy = nxt + (size_t)kFwdMax * 2;              // u32 [kTile]   y << 16 | x
+  static constexpr size_t region_a = sxy + (size_t)kTile * 4;
+  // reduction-phase aliases of region A
+  static constexpr size_t stile = 0;                                    // uint4 [kTile]
+  static constexpr size_t mem = stile + (size_t)kTile * 16;             // u16   [kTile]
+  static constexpr size_t big = mem + (size_t)kTile * 2;                // u16   [kTile]
+  static constexpr size_t mlabel = big + (size_t)kTile * 2;             // u32   [kTile]
+  static_assert(mlabel + (size_t)kTile * 4 <= region_a, "reduction arrays alias region A");
+  static constexpr size_t hb = region_a;                                // uint2 [kBackCap]
+  static constexpr size_t par = hb + (size_t)kBackCap * 8;              // u32   [kFwdMax]
+  static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile/2] (u16 pairs)
+  static constexpr size_t crank = csize + (size_t)kTile * 2;            // u16   [kTile]
+  static constexpr size_t coff = crank + (size_t)kTile * 2;             // u16   [kTile]
+  static constexpr size_t eb = coff + (size_t)kTile * 2;                // u16   [kEdgeBuf * threads]
+  static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2;
+  static constexpr size_t ccur = eb;                                    // u32   [kTile]   (alias)
+  static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
+  static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
+  static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
+  static constexpr size_t total = hflag + kTile;
+};
+template <class C>
+using tile_smem_layout = typename std::conditional<C::kHash, tile_smem_hash<C>, tile_smem_buckets<C>>::type;
 template <class C>
 constexpr size_t tile_smem_bytes() {
   return tile_smem_layout<C>::total;
@@ -279,21 +321,39 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
   using SL = tile_smem_layout<C>;
   constexpr int kStageItems = C::kStageItems;
   extern __shared__ __align__(16) unsigned char sm[];
-  uint2* csort = reinterpret_cast<uint2*>(sm + SL::csort);      // (toa - base, y<<16|x), bucket-sorted
-  uint32_t* ckey = reinterpret_cast<uint32_t*>(sm + SL::ckey);  // y << 16 | local index of csort entries
-  uint16_t* myrank = reinterpret_cast<uint16_t*>(sm + SL::myrank);  // local index -> csort position
+  // index arrays of the two configurations (only one set is used):
+  // sparse -- column buckets ranked by (row, time); dense -- pixel hash
+  uint2* csort = nullptr;     // (toa - base, y<<16|x), bucket-sorted
+  uint32_t* ckey = nullptr;   // y << 16 | local index of csort entries
+  uint16_t* myrank = nullptr; // local index -> csort position
+  uint32_t* bs = nullptr;     // bucket counts, then bucket starts
+  uint32_t* cltmp = nullptr;  // unranked bucket entries (alias of par)
+  uint32_t* tab = nullptr;    // pixel hash: pixel << 12 | list head, open addressing
+  uint32_t* stoa = nullptr;   // toa - base by local index
+  uint16_t* nxt = nullptr;    // next local index on the same pixel
+  uint32_t* sxy = nullptr;    // y << 16 | x of tile hits
+  if constexpr (C::kHash) {
+    tab = reinterpret_cast<uint32_t*>(sm + SL::tab);
+    stoa = reinterpret_cast<uint32_t*>(sm + SL::stoa);
+    nxt = reinterpret_cast<uint16_t*>(sm + SL::nxt);
+    sxy = reinterpret_cast<uint32_t*>(sm + SL::sxy);
+  } else {
+    csort = reinterpret_cast<uint2*>(sm + SL::csort);
+    ckey = reinterpret_cast<uint32_t*>(sm + SL::ckey);
+    myrank = reinterpret_cast<uint16_t*>(sm + SL::myrank);
+    bs = reinterpret_cast<uint32_t*>(sm + SL::bs);
+    cltmp = reinterpret_cast<uint32_t*>(sm + SL::cltmp);
+  }
   uint4* stile = reinterpret_cast<uint4*>(sm + SL::stile);      // tile hits (toa - base, xy, tot, idx)
   uint16_t* mem = reinterpret_cast<uint16_t*>(sm + SL::mem);    // member array grouped by component
   uint16_t* big = reinterpret_cast<uint16_t*>(sm + SL::big);    // roots of large components
   uint2* hb = reinterpret_cast<uint2*>(sm + SL::hb);            // back halo, index order
   uint32_t* mlabel = reinterpret_cast<uint32_t*>(sm + SL::mlabel);  // label by tile root (reductions)
-  uint32_t* bs = reinterpret_cast<uint32_t*>(sm + SL::bs);      // bucket counts, then bucket starts
   uint32_t* par = reinterpret_cast<uint32_t*>(sm + SL::par);
   uint32_t* csize2 = reinterpret_cast<uint32_t*>(sm + SL::csize);  // component sizes, two u16 per word
   uint16_t* crank = reinterpret_cast<uint16_t*>(sm + SL::crank);  // stage rank by root
   uint16_t* coff = reinterpret_cast<uint16_t*>(sm + SL::coff);    // member offset by root
   uint16_t* eb = reinterpret_cast<uint16_t*>(sm + SL::eb);
-  uint32_t* cltmp = reinterpret_cast<uint32_t*>(sm + SL::cltmp);
   uint32_t* ccur = reinterpret_cast<uint32_t*>(sm + SL::ccur);
   uint8_t* copen = sm + SL::copen;
   uint8_t* hflag = sm + SL::hflag;  // per tile hit: bit0 open mark, bit1 overflow
@@ -345,7 +405,11 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
     const uint64_t tp = srec_toa(p), tq = srec_toa(q);
     if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&a.hdr->sort_bad, 1u);
   }
-  for (uint32_t b = threadIdx.x; b < kBuckets + 4; b += kTileThreads) bs[b] = 0;
+  if constexpr (C::kHash) {
+    for (uint32_t b = threadIdx.x; b < (uint32_t)C::kSlots; b += kTileThreads) tab[b] = 0xffffffffu;
+  } else {
+    for (uint32_t b = threadIdx.x; b < kBuckets + 4; b += kTileThreads) bs[b] = 0;
+  }
   for (uint32_t j = threadIdx.x; j < kTile; j += kTileThreads) {
     copen[j] = 0;
     hflag[j] = 0;
@@ -362,64 +426,9 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
   const uint32_t nf = m - nt;
   const uint32_t dt32 = dt > 0xffffffffull ? 0xffffffffu : (uint32_t)dt;  // rel. ToAs differ by < 2^32
 
-  // ---- stage: back halo, and tile + forward halo counted into column buckets
-  // (sparse config: the 8 staged words per thread stay in registers; dense
-  // config: slots go to shared memory and S is re-read from L2)
-  constexpr int kRegItems = C::kRegStage ? kStageItems : 1;
-  uint2 ev[kRegItems];
-  uint32_t eslot[kRegItems];
-  uint16_t* eslot_s = reinterpret_cast<uint16_t*>(sm + SL::eslot);
-  auto staged = [&](uint32_t l) {
-    const srec r = load_srec(S + t0 + l);
-    return make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-  };
-  if (!wide) {
-    for (uint32_t k = threadIdx.x; k < nb; k += kTileThreads) {
-      const srec r = load_srec(S + b0 + k);
-      hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-    }
-    if constexpr (C::kRegStage) {
-#pragma unroll
-      for (int q = 0; q < kStageItems; ++q) {
-        const uint32_t l = threadIdx.x + q * kTileThreads;
-        if (l < m) {
-          ev[q] = staged(l);
-          eslot[q] = atomicAdd(bs + (ev[q].y & 0xffffu), 1u);
-        }
-      }
-    } else {
-      for (uint32_t l = threadIdx.x; l < m; l += kTileThreads)
-        eslot_s[l] = (uint16_t)atomicAdd(bs + (staged(l).y & 0xffffu), 1u);
-    }
-  }
-  __syncthreads();
-  // exclusive scan of the bucket counts (in place), longest bucket
-  if (!wide) {
-    constexpr int PT = kBuckets / kTileThreads;  // buckets per thread
-    uint32_t cnts[PT];
-    uint32_t s = 0, mx = 0;
-#pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      cnts[i] = bs[threadIdx.x * PT + i];
-      s += cnts[i];
-      mx = max(mx, cnts[i]);
-    }
-    mx = __reduce_max_sync(kFull, mx);
-    if (lane == 0) atomicMax(&s_bmax, mx);
-    uint32_t tot;
-    uint32_t ex = tile_block_scan(s, &tot, s_wsum);
-#pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      bs[threadIdx.x * PT + i] = ex;
-      ex += cnts[i];
-    }
-    if (threadIdx.x == 0) bs[kBuckets] = m;
-  }
-  __syncthreads();
-  TPX_PHASE(1);
-  if (s_bmax > (uint32_t)kBucketCap) wide = true;  // degenerate column: global path
-
-  if (wide) {
+  const uint32_t W = a.width;
+  auto slot_of_pixel = [&](uint32_t pix) { return (pix * 0x9E3779B1u) >> (32 - C::kSlotBits); };
+  auto run_wide = [&]() {
     // Every hit becomes its own open component; the global pass does the work.
     for (uint32_t j = threadIdx.x; j < kTile; j += kTileThreads) {
       const bool v = j < nt;
@@ -443,59 +452,184 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
       }
     }
     if (threadIdx.x == 0) a.comp_count[blockIdx.x] = nt;
-    return;
-  }
-
-  // ---- unordered scatter into column buckets, then rank inside each bucket
-  // by (row, time): key = y << 16 | local index (local index order = ToA order)
-  auto rank_in_bucket = [&](uint32_t l, uint2 e) {
-    const uint32_t b = e.y & 0xffffu;
-    const uint32_t key = (e.y & 0xffff0000u) | l;
-    const uint32_t s0 = bs[b], s1 = bs[b + 1];
-    uint32_t r = 0;
-    for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < key;
-    const uint32_t fin = s0 + r;
-    csort[fin] = e;
-    ckey[fin] = key;
-    myrank[l] = (uint16_t)fin;
   };
-  if constexpr (C::kRegStage) {
-#pragma unroll
-    for (int q = 0; q < kStageItems; ++q) {
-      const uint32_t l = threadIdx.x + q * kTileThreads;
-      if (l < m) cltmp[bs[ev[q].y & 0xffffu] + eslot[q]] = (ev[q].y & 0xffff0000u) | l;
+
+  if constexpr (!C::kHash) {
+    // ---- stage: back halo, and tile + forward halo counted into column buckets
+    // (sparse config: the 8 staged words per thread stay in registers; dense
+    // config: slots go to shared memory and S is re-read from L2)
+    constexpr int kRegItems = C::kRegStage ? kStageItems : 1;
+    uint2 ev[kRegItems];
+    uint32_t eslot[kRegItems];
+    uint16_t* eslot_s = reinterpret_cast<uint16_t*>(sm + SL::eslot);
+    auto staged = [&](uint32_t l) {
+      const srec r = load_srec(S + t0 + l);
+      return make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
+    };
+    if (!wide) {
+      for (uint32_t k = threadIdx.x; k < nb; k += kTileThreads) {
+        const srec r = load_srec(S + b0 + k);
+        hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
+      }
+      if constexpr (C::kRegStage) {
+  #pragma unroll
+        for (int q = 0; q < kStageItems; ++q) {
+          const uint32_t l = threadIdx.x + q * kTileThreads;
+          if (l < m) {
+            ev[q] = staged(l);
+            eslot[q] = atomicAdd(bs + (ev[q].y & 0xffffu), 1u);
+          }
+        }
+      } else {
+        for (uint32_t l = threadIdx.x; l < m; l += kTileThreads)
+          eslot_s[l] = (uint16_t)atomicAdd(bs + (staged(l).y & 0xffffu), 1u);
+      }
     }
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kStageItems; ++q) {
-      const uint32_t l = threadIdx.x + q * kTileThreads;
-      if (l < m) rank_in_bucket(l, ev[q]);
-    }
-  } else {
-    for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
-      const uint2 e = staged(l);
-      cltmp[bs[e.y & 0xffffu] + eslot_s[l]] = (e.y & 0xffff0000u) | l;
+    // exclusive scan of the bucket counts (in place), longest bucket
+    if (!wide) {
+      constexpr int PT = kBuckets / kTileThreads;  // buckets per thread
+      uint32_t cnts[PT];
+      uint32_t s = 0, mx = 0;
+  #pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        cnts[i] = bs[threadIdx.x * PT + i];
+        s += cnts[i];
+        mx = max(mx, cnts[i]);
+      }
+      mx = __reduce_max_sync(kFull, mx);
+      if (lane == 0) atomicMax(&s_bmax, mx);
+      uint32_t tot;
+      uint32_t ex = tile_block_scan(s, &tot, s_wsum);
+  #pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        bs[threadIdx.x * PT + i] = ex;
+        ex += cnts[i];
+      }
+      if (threadIdx.x == 0) bs[kBuckets] = m;
     }
     __syncthreads();
-    for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) rank_in_bucket(l, staged(l));
+    TPX_PHASE(1);
+    if (s_bmax > (uint32_t)kBucketCap) wide = true;  // degenerate column: global path
+
+
+    if (wide) {
+      run_wide();
+      return;
+    }
+    // ---- unordered scatter into column buckets, then rank inside each bucket
+    // by (row, time): key = y << 16 | local index (local index order = ToA order)
+    auto rank_in_bucket = [&](uint32_t l, uint2 e) {
+      const uint32_t b = e.y & 0xffffu;
+      const uint32_t key = (e.y & 0xffff0000u) | l;
+      const uint32_t s0 = bs[b], s1 = bs[b + 1];
+      uint32_t r = 0;
+      for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < key;
+      const uint32_t fin = s0 + r;
+      csort[fin] = e;
+      ckey[fin] = key;
+      myrank[l] = (uint16_t)fin;
+    };
+    if constexpr (C::kRegStage) {
+  #pragma unroll
+      for (int q = 0; q < kStageItems; ++q) {
+        const uint32_t l = threadIdx.x + q * kTileThreads;
+        if (l < m) cltmp[bs[ev[q].y & 0xffffu] + eslot[q]] = (ev[q].y & 0xffff0000u) | l;
+      }
+      __syncthreads();
+  #pragma unroll
+      for (int q = 0; q < kStageItems; ++q) {
+        const uint32_t l = threadIdx.x + q * kTileThreads;
+        if (l < m) rank_in_bucket(l, ev[q]);
+      }
+    } else {
+      for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
+        const uint2 e = staged(l);
+        cltmp[bs[e.y & 0xffffu] + eslot_s[l]] = (e.y & 0xffff0000u) | l;
+      }
+      __syncthreads();
+      for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) rank_in_bucket(l, staged(l));
+    }
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;  // par aliases cltmp
+    __syncthreads();
+
   }
-  __syncthreads();
-  for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;  // par aliases cltmp
-  __syncthreads();
+  if constexpr (C::kHash) {
+    // ---- stage: back halo; tile + forward halo into a pixel hash index.  Each
+    // occupied pixel owns one open-addressing slot (pixel << 12 | head) and a
+    // list of its local indices threaded through nxt[] -- a compact, per-CTA
+    // stand-in for the paper's 256x256 "last hit per pixel" matrix (P:171,
+    // P:310).  Inserts are lock-free pushes (atomicCAS on the slot word).
+    auto staged = [&](uint32_t l) {
+      const srec r = load_srec(S + t0 + l);
+      return make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
+    };
+    auto insert = [&](uint32_t l, uint2 e) {
+      stoa[l] = e.x;
+      if (l < nt) sxy[l] = e.y;
+      par[l] = l;
+      const uint32_t pix = (e.y >> 16) * W + (e.y & 0xffffu);
+      uint32_t h = slot_of_pixel(pix);
+      uint32_t cur = tab[h];
+      for (;;) {
+        const uint32_t ck = cur >> 12;
+        if (ck != kPixEmpty && ck != pix) {  // another pixel: linear probing
+          h = (h + 1) & (C::kSlots - 1);
+          cur = tab[h];
+          continue;
+        }
+        nxt[l] = ck == pix ? (uint16_t)(cur & 0xfffu) : kNil;
+        const uint32_t old = atomicCAS(tab + h, cur, (pix << 12) | l);
+        if (old == cur) break;
+        cur = old;
+      }
+    };
+    if (!wide) {
+      for (uint32_t k = threadIdx.x; k < nb; k += kTileThreads) {
+        const srec r = load_srec(S + b0 + k);
+        hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
+      }
+      if constexpr (C::kRegStage) {
+        uint2 ev[kStageItems];
+  #pragma unroll
+        for (int q = 0; q < kStageItems; ++q) {  // all loads first, then the inserts
+          const uint32_t l = threadIdx.x + q * kTileThreads;
+          if (l < m) ev[q] = staged(l);
+        }
+  #pragma unroll
+        for (int q = 0; q < kStageItems; ++q) {
+          const uint32_t l = threadIdx.x + q * kTileThreads;
+          if (l < m) insert(l, ev[q]);
+        }
+      } else {
+        for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) insert(l, staged(l));
+      }
+    }
+    __syncthreads();
+    TPX_PHASE(1);
+
+
+    if (wide) {
+      run_wide();
+      return;
+    }
+  }
   TPX_PHASE(2);
 
   // ---- pixel-exact neighbour search.  For a hit at (x, y) with local index j
   // only the FIRST later hit on each of its 9 neighbouring pixels needs an edge
   // (later hits on that pixel are within dt of the first one and reach it via
   // their own same-pixel edge; this is the paper's last-hit-per-pixel rule,
-  // P:171, read forwards).  Column x' in {x-1, x, x+1} is a bucket
-  // sorted by (row, time): one binary search finds row y-1 after j, then a
-  // short walk over rows y-1..y+1 takes the first entry per row with local
-  // index > j and tests it against dt.  Work per hit is independent of the
-  // window density (dense heavy-ion windows included).
+  // P:171, read forwards).  Sparse: column x' in {x-1, x, x+1} is a
+  // bucket sorted by (row, time); one binary search finds row y-1 after j,
+  // then a short walk over rows y-1..y+1 takes the first entry per row with
+  // local index > j.  Dense: per neighbouring pixel one hash probe sequence,
+  // then the smallest local index > j in its list.  Either way the work per
+  // hit is independent of the window density.
   const uint64_t prev_last = s_meta[5];
   const uint64_t first_unstaged = s_meta[4];
-  const uint32_t wmax = a.width - 1;
+  const uint32_t wmax = W - 1;
   const uint32_t n_chunks = (nt + 31) / 32;
   for (;;) {
     uint32_t chunk = 0;
@@ -505,40 +639,69 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
     const uint32_t j = chunk * 32 + lane;
     uint32_t ne = 0;
     if (j < nt) {
-      const uint2 h = csort[myrank[j]];
-      const uint32_t x = h.y & 0xffffu, y = h.y >> 16;
-      const uint32_t xlo = x ? x - 1 : 0, xhi = x < wmax ? x + 1 : x;
-      const uint32_t ylo = y ? y - 1 : 0, yhi = y + 1;
-      const uint32_t k0 = (ylo << 16) | j;  // first key of interest: row ylo, index > j
-      for (uint32_t b = xlo; b <= xhi; ++b) {
-        uint32_t lo = bs[b], hi = bs[b + 1];
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (ckey[mid] <= k0) lo = mid + 1; else hi = mid;
+      uint32_t xy, tj;
+      auto edge = [&](uint32_t lj) {
+        if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
+        else s_unite(par, j, lj);
+      };
+      if constexpr (C::kHash) {
+        xy = sxy[j];
+        tj = stoa[j];
+        const uint32_t x = xy & 0xffffu, y = xy >> 16;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx) {
+            if ((dy < 0 && y == 0) || (dx < 0 && x == 0) || (dx > 0 && x == wmax)) continue;
+            // row y + 1 == height gives a pixel id >= W * H: never present
+            const uint32_t pix = (y + dy) * W + (x + dx);
+            uint32_t h = slot_of_pixel(pix);
+            uint32_t cur;
+            while (((cur = tab[h]) >> 12) != pix) {
+              if ((cur >> 12) == kPixEmpty) break;
+              h = (h + 1) & (C::kSlots - 1);
+            }
+            if ((cur >> 12) != pix) continue;
+            uint32_t best = 0xffffu;
+            for (uint32_t q = cur & 0xfffu; q != kNil; q = nxt[q])
+              if (q > j && q < best) best = q;
+            if (best != 0xffffu && stoa[best] - tj <= dt32) edge(best);
+          }
         }
-        uint32_t taken = 0xffffffffu;  // row whose first later hit was already taken
-        for (uint32_t p = lo; p < bs[b + 1]; ++p) {
-          const uint32_t k = ckey[p];
-          const uint32_t row = k >> 16;
-          if (row > yhi) break;
-          if (row == taken || (k & 0xffffu) <= j) continue;
-          taken = row;
-          if (csort[p].x - h.x <= dt32) {
-            const uint32_t lj = k & 0xffffu;
-            if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
-            else s_unite(par, j, lj);
+      } else {
+        const uint2 h = csort[myrank[j]];
+        xy = h.y;
+        tj = h.x;
+        const uint32_t x = h.y & 0xffffu, y = h.y >> 16;
+        const uint32_t xlo = x ? x - 1 : 0, xhi = x < wmax ? x + 1 : x;
+        const uint32_t ylo = y ? y - 1 : 0, yhi = y + 1;
+        const uint32_t k0 = (ylo << 16) | j;  // first key of interest: row ylo, index > j
+        for (uint32_t b = xlo; b <= xhi; ++b) {
+          uint32_t lo = bs[b], hi = bs[b + 1];
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ckey[mid] <= k0) lo = mid + 1; else hi = mid;
+          }
+          uint32_t taken = 0xffffffffu;  // row whose first later hit was already taken
+          for (uint32_t p = lo; p < bs[b + 1]; ++p) {
+            const uint32_t k = ckey[p];
+            const uint32_t row = k >> 16;
+            if (row > yhi) break;
+            if (row == taken || (k & 0xffffu) <= j) continue;
+            taken = row;
+            if (csort[p].x - h.x <= dt32) edge(k & 0xffffu);
           }
         }
       }
       uint8_t fl = 0;
-      if (ftrunc && first_unstaged <= base + h.x + dt) fl = 3;  // window continues past the halo
-      if (t0 > 0 && base + h.x <= prev_last + dt) {           // could an earlier tile reach it?
+      if (ftrunc && first_unstaged <= base + tj + dt) fl = 3;  // window continues past the halo
+      if (t0 > 0 && base + tj <= prev_last + dt) {           // could an earlier tile reach it?
         bool found = false;
         int lb = (int)nb - 1;
         for (; lb >= 0; --lb) {
           const uint2 g = hb[lb];
-          if (h.x - g.x > dt32) break;
-          if (adjacent(h.y, g.y)) {
+          if (tj - g.x > dt32) break;
+          if (adjacent(xy, g.y)) {
             found = true;
             break;
           }

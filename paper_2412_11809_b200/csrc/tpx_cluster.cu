@@ -275,6 +275,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.n = r.n;
   a.dt = c->dt;
   a.width = c->width;
+  a.height = c->height;
   a.n_owned = (uint32_t)r.n_owned;
   a.labels = r.labels;
   a.parent_g = parent_g;
@@ -517,9 +518,11 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
     c->stats.sort_retries = attempt < 2 ? attempt : 2;
-    // the tile kernel indexes one bucket per pixel column: wider sensors take
-    // the global union-find pipeline
-    rc = (attempt == 3 || c->width > (uint32_t)kBuckets) ? cluster_global(c, r) : cluster_sorted(c, r);
+    // the tile kernel indexes one bucket per pixel column (sparse) or packs
+    // pixel ids in 20 bits (dense): larger sensors take the global pipeline
+    const bool big_sensor =
+        c->width > (uint32_t)kBuckets || (uint64_t)c->width * c->height + c->width > kMaxTilePixels;
+    rc = (attempt == 3 || big_sensor) ? cluster_global(c, r) : cluster_sorted(c, r);
     if (rc) return rc;
     if ((rc = read_header(c, r))) return rc;
     const dev_hdr& h = *c->host_hdr;

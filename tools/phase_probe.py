@@ -16,7 +16,7 @@ for _ in range(2):
 c.set_profiling(2)
 c.run(d)
 st = c.stats()
-names = ["meta", "stage+bucket", "scatter+rank", "search+union", "flatten", "sizes+pairs", "compact", "features", "outputs"]
+names = ["meta", "stage+index", "scatter+rank", "search+union", "flatten", "sizes+pairs", "compact", "features", "outputs"]
 cyc = st["tile_phase_cycles"][:9]
 tot = sum(cyc) or 1
 print(preset, n, {k: round(v, 3) for k, v in st["stage_ms"].items()})
