@@ -21,6 +21,9 @@ namespace tpx {
 constexpr int kWSortThreads = 512;
 constexpr int kWSortWarps = kWSortThreads / 32;
 constexpr int kWSortTile = 4096;   // output records per CTA (T)
+constexpr int kWDigitBits = 9;     // radix digit: 512 bins, so a 18-bit window key takes 2 passes
+constexpr int kWRadix = 1 << kWDigitBits;
+static_assert(kWRadix <= kWSortThreads, "one scan thread per digit");
 
 template <int IT>
 struct wsort_cfg {
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);                       // [W]
   uint16_t* sval = reinterpret_cast<uint16_t*>(skey + C::W);                     // [W]
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(sval + C::W);                      // [256 * warps]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sval + C::W);                      // [kWRadix * warps]
   __shared__ unsigned long long red[33];
 
   const uint64_t k0 = (uint64_t)blockIdx.x * kWSortTile;
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
     return;
   }
   const int bits = range ? 64 - __clzll(range) : 0;
-  const int passes = (bits + 7) >> 3;
+  const int passes = (bits + kWDigitBits - 1) / kWDigitBits;
   uint32_t key[IT];
   uint32_t vl[IT];  // low 16 bits: window position (payload); high 16: rank within the warp
 #pragma unroll
@@ -116,20 +119,20 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
   }
 
   // ---- stable LSD radix passes, 8 bits each, ranks via warp-private counters
-  // cnt is warp-major (cnt[w * 256 + d]): lanes of a warp touch banks d % 32,
+  // cnt is warp-major (cnt[w * kWRadix + d]): lanes of a warp touch banks d % 32,
   // so counter traffic is (nearly) conflict-free; equal digits are grouped by
   // __match_any_sync and only the group leader writes.
   __shared__ uint32_t dsum[kWSortThreads / 32];
   for (int pass = 0; pass < passes || pass == 0; ++pass) {
-    const int shift = pass * 8;
-    for (int i = threadIdx.x; i < 256 * kWSortWarps; i += kWSortThreads) cnt[i] = 0;
+    const int shift = pass * kWDigitBits;
+    for (int i = threadIdx.x; i < kWRadix * kWSortWarps; i += kWSortThreads) cnt[i] = 0;
     __syncthreads();
-    uint32_t* wc = cnt + warp * 256;
+    uint32_t* wc = cnt + warp * kWRadix;
 #pragma unroll
     for (int r = 0; r < IT; ++r) {
       const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
       const bool valid = p < m;
-      const unsigned d = valid ? (key[r] >> shift) & 0xffu : 256u;
+      const unsigned d = valid ? (key[r] >> shift) & (kWRadix - 1) : (unsigned)kWRadix;
       const unsigned peers = __match_any_sync(kFull, d);
       uint32_t b = 0;
       if (valid) b = wc[d];
@@ -139,14 +142,14 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
       __syncwarp();
     }
     __syncthreads();
-    // offsets in (digit, warp) order: thread d < 256 owns digit d
+    // offsets in (digit, warp) order: thread d < kWRadix owns digit d
     {
       uint32_t tot = 0;
-      if (threadIdx.x < 256) {
+      if (threadIdx.x < kWRadix) {
 #pragma unroll
-        for (int w = 0; w < kWSortWarps; ++w) tot += cnt[w * 256 + threadIdx.x];
+        for (int w = 0; w < kWSortWarps; ++w) tot += cnt[w * kWRadix + threadIdx.x];
       }
-      uint32_t x = tot;  // inclusive scan of digit totals over threads 0..255 (warps 0..7)
+      uint32_t x = tot;  // inclusive scan of digit totals over threads 0..kWRadix-1
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(kFull, x, o);
@@ -154,13 +157,13 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
       }
       if (lane == 31) dsum[warp] = x;
       __syncthreads();
-      if (threadIdx.x < 256) {
+      if (threadIdx.x < kWRadix) {
         uint32_t basev = x - tot;
         for (unsigned w2 = 0; w2 < warp; ++w2) basev += dsum[w2];
 #pragma unroll
         for (int w = 0; w < kWSortWarps; ++w) {
-          const uint32_t c = cnt[w * 256 + threadIdx.x];
-          cnt[w * 256 + threadIdx.x] = basev;
+          const uint32_t c = cnt[w * kWRadix + threadIdx.x];
+          cnt[w * kWRadix + threadIdx.x] = basev;
           basev += c;
         }
       }
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
     for (int r = 0; r < IT; ++r) {
       const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
       if (p < m) {
-        const unsigned d = (key[r] >> shift) & 0xffu;
+        const unsigned d = (key[r] >> shift) & (kWRadix - 1);
         const uint32_t q = wc[d] + (vl[r] >> 16);
         skey[q] = key[r];
         sval[q] = (uint16_t)vl[r];
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
 
 template <int IT>
 constexpr size_t window_sort_smem() {
-  return (size_t)wsort_cfg<IT>::W * 6 + 256 * kWSortWarps * 4;
+  return (size_t)wsort_cfg<IT>::W * 6 + (size_t)kWRadix * kWSortWarps * 4;
 }
 
 }  // namespace tpx
