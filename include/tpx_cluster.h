@@ -462,6 +462,30 @@ int tpx_stream_pop(tpx_stream* s, tpx_stream_batch* out);
 int tpx_stream_get_stats(const tpx_stream* s, tpx_stream_stats* out);
 void tpx_stream_destroy(tpx_stream* s);
 
+/* One-shot host-to-host run of a whole stream held in host memory -- the
+ * paper's GPU benchmark clock (§5 l.278-280: from a populated host
+ * buffer until the clustered data is back on the host).  Same BufFill
+ * decisions, carry and results as tpx_stream_push + flush, without host-side
+ * copies of the input (runs go to the device straight from hits_host, which
+ * should be pinned), and with copy/compute overlap across buffers (l.310).
+ *   hits_host     HOST, n < 2^32 - 1 hits in arrival order.
+ *   order_out     HOST, n u32: arrival indices, cluster blocks back to back
+ *                 (buffer after buffer, Step-6 order inside a buffer).
+ *   clusters_out  HOST, `capacity` records; offset = position in order_out.
+ *   n_clusters_out HOST: number of clusters (TPX_ERR_CAPACITY if > capacity;
+ *                 the first `capacity` records are written).
+ *   workspace     DEVICE, >= tpx_stream_run_host_workspace_bytes(cfg).
+ *   stats_out     HOST, may be NULL; device_ms = first H2D to last D2H.
+ * Synchronous: returns when every result is in host memory. */
+int tpx_stream_run_host_workspace_bytes(const tpx_stream_config* cfg,
+                                        size_t* bytes);
+int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits_host,
+                        uint64_t n, uint32_t* order_out,
+                        tpx_stream_cluster* clusters_out, uint64_t capacity,
+                        uint64_t* n_clusters_out, void* workspace,
+                        size_t workspace_bytes, void* cuda_stream,
+                        tpx_stream_stats* stats_out);
+
 /* Host-only helper (no GPU): the buffer each hit is sent in by Alg. "Hit
  * buffer filling" (buffer_id_out[n], HOST) and each buffer's cut (cuts_out,
  * HOST, cuts_cap entries; the final buffer's cut is UINT64_MAX), exactly as

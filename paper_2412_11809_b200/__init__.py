@@ -342,6 +342,9 @@ _stream_flush = _proto("tpx_stream_flush", _int, _vp)
 _stream_pop = _proto("tpx_stream_pop", _int, _vp, ctypes.POINTER(StreamBatch))
 _stream_stats = _proto("tpx_stream_get_stats", _int, _vp, ctypes.POINTER(StreamStats))
 _stream_destroy = _proto("tpx_stream_destroy", None, _vp)
+_stream_rh_ws = _proto("tpx_stream_run_host_workspace_bytes", _int, ctypes.POINTER(StreamConfig), _size_t_p)
+_stream_rh = _proto("tpx_stream_run_host", _int, ctypes.POINTER(StreamConfig), _vp, _u64, _vp, _vp, _u64,
+                    ctypes.POINTER(_u64), _vp, ctypes.c_size_t, _vp, ctypes.POINTER(StreamStats))
 _buffill_assign = _proto("tpx_buffill_assign", _int, _vp, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _u64,
                          ctypes.POINTER(_u64))
 
@@ -358,6 +361,43 @@ def buffill_assign(hits: np.ndarray, b: int, b_t: int, t: int, t_closing: int):
     _check(_buffill_assign(h.ctypes.data if n else None, n, int(b), int(b_t), int(t), int(t_closing),
                            ids.ctypes.data, cuts.ctypes.data, cap, ctypes.byref(nb)), "tpx_buffill_assign")
     return ids[:n], [int(c) for c in cuts[: nb.value]]
+
+
+class StreamRunner:
+    """``tpx_stream_run_host``: one-shot host-to-host clustering of a whole
+    stream in host memory (BufFill + exact carry, copy/compute overlap)."""
+
+    def __init__(self, dt_max: int, buffer_hits: int, reserve_hits: int, disorder_ticks: int, closing_ticks: int,
+                 max_device_hits: int | None = None, width: int = 256, height: int = 256):
+        torch = _torch()
+        self.cfg = StreamConfig(int(dt_max), int(width), int(height), int(buffer_hits), int(reserve_hits),
+                                int(disorder_ticks), int(closing_ticks),
+                                int(max_device_hits or 2 * (buffer_hits + reserve_hits)))
+        b = ctypes.c_size_t(0)
+        _check(_stream_rh_ws(ctypes.byref(self.cfg), ctypes.byref(b)), "tpx_stream_run_host_workspace_bytes")
+        self._ws = torch.empty(max(b.value, 256), dtype=torch.uint8, device="cuda")
+        self.last_stats = None
+
+    @staticmethod
+    def _ptr(a):
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+    def run(self, hits_host, order_out, clusters_out, capacity: int | None = None, stream=None) -> int:
+        """hits_host: (pinned) CPU tensor / numpy array of n 16-byte hits;
+        order_out: n u32; clusters_out: capacity x 80 bytes.  Returns k."""
+        nb = hits_host.numel() * hits_host.element_size() if hasattr(hits_host, "numel") else hits_host.nbytes
+        n = nb // 16
+        if capacity is None:
+            cb = clusters_out.numel() * clusters_out.element_size() if hasattr(clusters_out, "numel") \
+                else clusters_out.nbytes
+            capacity = cb // 80
+        k = _u64(0)
+        st = StreamStats()
+        _check(_stream_rh(ctypes.byref(self.cfg), self._ptr(hits_host), int(n), self._ptr(order_out),
+                          self._ptr(clusters_out), int(capacity), ctypes.byref(k), self._ws.data_ptr(),
+                          self._ws.numel(), _stream_handle(stream), ctypes.byref(st)), "tpx_stream_run_host")
+        self.last_stats = {f: getattr(st, f) for f, _ in StreamStats._fields_}
+        return k.value
 
 
 class Stream:

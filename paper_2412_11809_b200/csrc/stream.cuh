@@ -88,17 +88,25 @@ struct stream_emit_args {
   const uint32_t* hoff;         // closed block -> output hit offset
   uint64_t k;
   tpx_stream_cluster* out_cl;
-  tpx_hit* out_hits;
-  uint64_t* out_g;
+  tpx_hit* out_hits;            // may be null (one-shot run: the caller has the hits)
+  uint64_t* out_g;              // arrival index per output hit (u64), or null
+  uint32_t* out_g32;            // arrival index per output hit (u32), or null
+  uint64_t hoff_base;           // added to record offsets (one-shot: position in order_out)
   uint32_t* open_flag;          // per local position: hit of an open cluster
 };
+
+__device__ __forceinline__ void stream_put_hit(const stream_emit_args& a, uint64_t q, uint32_t p) {
+  if (a.out_hits) reinterpret_cast<uint4*>(a.out_hits)[q] = reinterpret_cast<const uint4*>(a.hits)[p];
+  if (a.out_g) a.out_g[q] = a.gidx[p];
+  if (a.out_g32) a.out_g32[q] = (uint32_t)a.gidx[p];
+}
 
 __device__ __forceinline__ void stream_block_head(const stream_emit_args& a, uint64_t g) {
   const uint32_t c = a.cluster_of[g];
   const tpx_cluster_features f = a.feats[c];
   tpx_stream_cluster r;
   r.label = a.gidx[f.label];  // smallest local position = smallest arrival index
-  r.offset = a.hoff[g];
+  r.offset = a.hoff_base + a.hoff[g];
   r.size = f.size;
   r.reserved = 0;
   r.toa_min = f.toa_min;
@@ -122,11 +130,7 @@ __global__ void k_stream_emit_small(stream_emit_args a) {
     if (a.closed_flag[g]) {
       stream_block_head(a, g);
       const uint64_t h0 = a.hoff[g];
-      for (uint32_t j = o0; j < o1; ++j) {
-        const uint32_t p = a.order[j];
-        reinterpret_cast<uint4*>(a.out_hits)[h0 + (j - o0)] = reinterpret_cast<const uint4*>(a.hits)[p];
-        a.out_g[h0 + (j - o0)] = a.gidx[p];
-      }
+      for (uint32_t j = o0; j < o1; ++j) stream_put_hit(a, h0 + (j - o0), a.order[j]);
     } else {
       for (uint32_t j = o0; j < o1; ++j) a.open_flag[a.order[j]] = 1u;
     }
@@ -148,16 +152,18 @@ __global__ void k_stream_emit_large(stream_emit_args a) {
       if (a.closed_flag[g]) {
         if (lane == 0) stream_block_head(a, g);
         const uint64_t h0 = a.hoff[g];
-        for (uint32_t j = o0 + lane; j < o1; j += 32) {
-          const uint32_t p = a.order[j];
-          reinterpret_cast<uint4*>(a.out_hits)[h0 + (j - o0)] = reinterpret_cast<const uint4*>(a.hits)[p];
-          a.out_g[h0 + (j - o0)] = a.gidx[p];
-        }
+        for (uint32_t j = o0 + lane; j < o1; j += 32) stream_put_hit(a, h0 + (j - o0), a.order[j]);
       } else {
         for (uint32_t j = o0 + lane; j < o1; j += 32) a.open_flag[a.order[j]] = 1u;
       }
     }
   }
+}
+
+// Arrival indices of a run of consecutive input hits.
+__global__ void k_iota64(uint64_t* __restrict__ g, uint64_t n, uint64_t base) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    g[i] = base + i;
 }
 
 // Carried hits in local (= arrival) order.
@@ -228,60 +234,47 @@ struct stream_batch_store {
   pinned_vec<uint64_t> g;
 };
 
-}  // namespace tpx
-
-struct tpx_stream {
-  tpx_stream_config cfg;
+// Device state of one stream: the carry and the per-buffer scratch.
+struct stream_dev {
   tpx_cluster* ctx = nullptr;
   cudaStream_t s = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  tpx::buffill_t<tpx::pinned_vec<tpx_hit>, tpx::pinned_vec<uint64_t>> bf;
-  uint64_t arrivals = 0, last_cut = 0, seq = 0;
-  bool have_cut = false, flushed = false;
-  // device regions (caller workspace)
-  char* ws = nullptr;
-  size_t ws_bytes = 0;
-  uint64_t cap = 0;  // device hits per buffer (new + carried)
-  tpx_hit *d_new = nullptr, *d_hits = nullptr, *d_carry = nullptr, *d_out_hits = nullptr;
-  uint64_t *d_new_g = nullptr, *d_g = nullptr, *d_carry_g = nullptr, *d_out_g = nullptr;
+  uint64_t cap = 0, dt = 0;
+  tpx_hit *d_hits = nullptr, *d_carry = nullptr;
+  uint64_t *d_g = nullptr, *d_carry_g = nullptr;
   uint32_t *d_labels = nullptr, *d_order = nullptr, *d_offsets = nullptr, *d_cluster_of = nullptr;
   uint32_t *d_flag = nullptr, *d_size = nullptr, *d_cidx = nullptr, *d_hoff = nullptr, *d_open = nullptr,
            *d_cpos = nullptr, *d_counts = nullptr, *d_partials = nullptr;
   tpx_cluster_features* d_feats = nullptr;
-  tpx_stream_cluster* d_out_cl = nullptr;
   char* d_run_ws = nullptr;
   size_t run_ws_bytes = 0;
   uint64_t n_carry = 0;
   uint32_t* h_counts = nullptr;  // pinned [4]
-  std::deque<tpx::stream_batch_store*> ready, pool;
-  tpx::stream_batch_store* current = nullptr;  // last popped batch (valid until the next pop)
-  tpx_stream_stats st;
 };
 
-namespace tpx {
-
-struct stream_layout {
-  size_t new_h, new_g, hits, g, carry, carry_g, out_hits, out_g, labels, order, offsets, cluster_of, flag, size, cidx,
-      hoff, open, cpos, counts, partials, feats, out_cl, run_ws, total;
+struct stream_out {
+  tpx_stream_cluster* cl;
+  tpx_hit* hits;
+  uint64_t* g;
+  uint32_t* g32;
+  uint64_t hoff_base;
 };
 
-static int stream_layout_of(const tpx_stream_config* cfg, stream_layout* L) {
-  const uint64_t cap = cfg->max_device_hits;
-  const uint64_t fresh = cfg->buffer_hits + cfg->reserve_hits;
-  size_t off = 0;
+// Shared scratch (bytes) of a stream_dev for `cap` device hits per buffer.
+struct stream_dev_layout {
+  size_t hits, g, carry, carry_g, labels, order, offsets, cluster_of, flag, size, cidx, hoff, open, cpos, counts,
+      partials, feats, run_ws, total;
+};
+
+static size_t stream_dev_layout_of(uint64_t cap, size_t off, stream_dev_layout* L) {
   auto take = [&](size_t bytes) {
     size_t o = off;
     off += align256(bytes);
     return o;
   };
-  L->new_h = take(fresh * 16);
-  L->new_g = take(fresh * 8);
   L->hits = take(cap * 16);
   L->g = take(cap * 8);
   L->carry = take(cap * 16);
   L->carry_g = take(cap * 8);
-  L->out_hits = take(cap * 16);
-  L->out_g = take(cap * 8);
   L->labels = take(cap * 4);
   L->order = take(cap * 4);
   L->offsets = take(cap * 4 + 4);
@@ -295,9 +288,140 @@ static int stream_layout_of(const tpx_stream_config* cfg, stream_layout* L) {
   L->counts = take(64);
   L->partials = take((size_t)n_tiles_of(cap, kScanTile) * 4 + 64);
   L->feats = take(cap * 64);
-  L->out_cl = take(cap * 80);
   L->run_ws = off;
-  L->total = off + align256(make_layout(cap).total);
+  off += align256(make_layout(cap).total);
+  L->total = off;
+  return off;
+}
+
+static void stream_dev_bind(stream_dev* d, char* w, const stream_dev_layout& L, size_t ws_end) {
+  d->d_hits = (tpx_hit*)(w + L.hits);
+  d->d_g = (uint64_t*)(w + L.g);
+  d->d_carry = (tpx_hit*)(w + L.carry);
+  d->d_carry_g = (uint64_t*)(w + L.carry_g);
+  d->d_labels = (uint32_t*)(w + L.labels);
+  d->d_order = (uint32_t*)(w + L.order);
+  d->d_offsets = (uint32_t*)(w + L.offsets);
+  d->d_cluster_of = (uint32_t*)(w + L.cluster_of);
+  d->d_flag = (uint32_t*)(w + L.flag);
+  d->d_size = (uint32_t*)(w + L.size);
+  d->d_cidx = (uint32_t*)(w + L.cidx);
+  d->d_hoff = (uint32_t*)(w + L.hoff);
+  d->d_open = (uint32_t*)(w + L.open);
+  d->d_cpos = (uint32_t*)(w + L.cpos);
+  d->d_counts = (uint32_t*)(w + L.counts);
+  d->d_partials = (uint32_t*)(w + L.partials);
+  d->d_feats = (tpx_cluster_features*)(w + L.feats);
+  d->d_run_ws = w + L.run_ws;
+  d->run_ws_bytes = ws_end - L.run_ws;
+}
+
+// One buffer on the device: merge the carried hits with the nn fresh ones
+// (device, arrival order), cluster + group, emit the closed clusters into
+// `out`, keep the open ones' hits as the next carry.  Returns the emitted
+// cluster and hit counts (one small read-back; all work on d->s).
+static int stream_pass(stream_dev* d, const tpx_hit* fresh, const uint64_t* fresh_g, uint64_t nn, uint64_t cut,
+                       bool final_buffer, const stream_out& out, uint64_t* kc_out, uint64_t* nh_out) {
+  tpx_cluster* c = d->ctx;
+  const uint64_t nc = d->n_carry;
+  const uint64_t n = nn + nc;
+  *kc_out = *nh_out = 0;
+  if (n == 0) return TPX_OK;
+  if (n > d->cap) return TPX_ERR_CAPACITY;
+  cudaStream_t st = d->s;
+  const tpx_hit* hits = fresh;
+  const uint64_t* gidx = fresh_g;
+  if (nc) {
+    k_stream_merge<<<grid_for(n, 256), 256, 0, st>>>(d->d_carry, d->d_carry_g, (uint32_t)nc, fresh, fresh_g,
+                                                      (uint32_t)nn, d->d_hits, d->d_g);
+    TPX_LAUNCHED(c);
+    hits = d->d_hits;
+    gidx = d->d_g;
+  }
+  uint64_t k = 0;
+  int rc = tpx_cluster_run_grouped(c, hits, n, d->d_labels, d->d_feats, nullptr, n, &k, d->d_order, d->d_offsets,
+                                   d->d_cluster_of, d->d_run_ws, d->run_ws_bytes, st);
+  if (rc) return rc;
+  const int gk = grid_for(k, 256), gn = grid_for(n, 256);
+  k_stream_blocks<<<gk, 256, 0, st>>>(d->d_cluster_of, d->d_feats, k, cut, d->dt, final_buffer ? 1 : 0, d->d_flag,
+                                      d->d_size);
+  TPX_LAUNCHED(c);
+  if ((rc = exclusive_scan(c, d->d_flag, k, d->d_cidx, d->d_partials, d->d_counts + 0, st))) return rc;
+  if ((rc = exclusive_scan(c, d->d_size, k, d->d_hoff, d->d_partials, d->d_counts + 1, st))) return rc;
+  TPX_CUDA(cudaMemsetAsync(d->d_open, 0, n * 4, st));
+  stream_emit_args a;
+  a.hits = hits;
+  a.gidx = gidx;
+  a.order = d->d_order;
+  a.offsets = d->d_offsets;
+  a.cluster_of = d->d_cluster_of;
+  a.feats = d->d_feats;
+  a.closed_flag = d->d_flag;
+  a.cidx = d->d_cidx;
+  a.hoff = d->d_hoff;
+  a.k = k;
+  a.out_cl = out.cl;
+  a.out_hits = out.hits;
+  a.out_g = out.g;
+  a.out_g32 = out.g32;
+  a.hoff_base = out.hoff_base;
+  a.open_flag = d->d_open;
+  k_stream_emit_small<<<gk, 256, 0, st>>>(a);
+  TPX_LAUNCHED(c);
+  k_stream_emit_large<<<gk, 256, 0, st>>>(a);
+  TPX_LAUNCHED(c);
+  if ((rc = exclusive_scan(c, d->d_open, n, d->d_cpos, d->d_partials, d->d_counts + 2, st))) return rc;
+  k_stream_carry<<<gn, 256, 0, st>>>(hits, gidx, n, d->d_open, d->d_cpos, d->d_carry, d->d_carry_g);
+  TPX_LAUNCHED(c);
+  TPX_CUDA(cudaMemcpyAsync(d->h_counts, d->d_counts, 12, cudaMemcpyDeviceToHost, st));
+  TPX_CUDA(cudaStreamSynchronize(st));
+  *kc_out = d->h_counts[0];
+  *nh_out = d->h_counts[1];
+  d->n_carry = d->h_counts[2];
+  return TPX_OK;
+}
+
+}  // namespace tpx
+
+struct tpx_stream {
+  tpx_stream_config cfg;
+  tpx::stream_dev dev;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  tpx::buffill_t<tpx::pinned_vec<tpx_hit>, tpx::pinned_vec<uint64_t>> bf;
+  uint64_t arrivals = 0, last_cut = 0, seq = 0;
+  bool have_cut = false, flushed = false;
+  tpx_hit* d_new = nullptr;
+  uint64_t* d_new_g = nullptr;
+  tpx_hit* d_out_hits = nullptr;
+  uint64_t* d_out_g = nullptr;
+  tpx_stream_cluster* d_out_cl = nullptr;
+  std::deque<tpx::stream_batch_store*> ready, pool;
+  tpx::stream_batch_store* current = nullptr;  // last popped batch (valid until the next pop)
+  tpx_stream_stats st;
+};
+
+namespace tpx {
+
+struct stream_layout {
+  size_t new_h, new_g, out_hits, out_g, out_cl, total;
+  stream_dev_layout dev;
+};
+
+static int stream_layout_of(const tpx_stream_config* cfg, stream_layout* L) {
+  const uint64_t cap = cfg->max_device_hits;
+  const uint64_t fresh = cfg->buffer_hits + cfg->reserve_hits;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  L->new_h = take(fresh * 16);
+  L->new_g = take(fresh * 8);
+  L->out_hits = take(cap * 16);
+  L->out_g = take(cap * 8);
+  L->out_cl = take(cap * 80);
+  L->total = stream_dev_layout_of(cap, off, &L->dev);
   return TPX_OK;
 }
 
@@ -308,64 +432,20 @@ static void stream_release(tpx_stream* s, stream_batch_store* b) {
 // Cluster the current buffer (bf.buf + carried hits) with cut `cut`; queue a
 // batch of the closed clusters; keep the open ones' hits on the device.
 static int stream_process(tpx_stream* s, uint64_t cut, bool final_buffer) {
-  tpx_cluster* c = s->ctx;
   const uint64_t nn = s->bf.buf.size();
-  const uint64_t nc = s->n_carry;
-  const uint64_t n = nn + nc;
-  if (n == 0) return TPX_OK;
-  if (nn > s->cfg.buffer_hits + s->cfg.reserve_hits || n > s->cap) return TPX_ERR_CAPACITY;
+  if (nn + s->dev.n_carry == 0) return TPX_OK;
+  if (nn > s->cfg.buffer_hits + s->cfg.reserve_hits) return TPX_ERR_CAPACITY;
   if (!s->bf.buf.ok || !s->bf.buf_g.ok) return TPX_ERR_OOM;
-  cudaStream_t st = s->s;
+  cudaStream_t st = s->dev.s;
   TPX_CUDA(cudaEventRecord(s->ev0, st));
-  const tpx_hit* hits = s->d_new;
-  const uint64_t* gidx = s->d_new_g;
   if (nn) {
     TPX_CUDA(cudaMemcpyAsync(s->d_new, s->bf.buf.p, nn * 16, cudaMemcpyHostToDevice, st));
     TPX_CUDA(cudaMemcpyAsync(s->d_new_g, s->bf.buf_g.p, nn * 8, cudaMemcpyHostToDevice, st));
   }
-  if (nc) {
-    k_stream_merge<<<grid_for(n, 256), 256, 0, st>>>(s->d_carry, s->d_carry_g, (uint32_t)nc, s->d_new, s->d_new_g,
-                                                      (uint32_t)nn, s->d_hits, s->d_g);
-    TPX_LAUNCHED(c);
-    hits = s->d_hits;
-    gidx = s->d_g;
-  }
-  uint64_t k = 0;
-  int rc = tpx_cluster_run_grouped(c, hits, n, s->d_labels, s->d_feats, nullptr, n, &k, s->d_order, s->d_offsets,
-                                   s->d_cluster_of, s->d_run_ws, s->run_ws_bytes, st);
+  stream_out out{s->d_out_cl, s->d_out_hits, s->d_out_g, nullptr, 0};
+  uint64_t kc = 0, nh = 0;
+  int rc = stream_pass(&s->dev, s->d_new, s->d_new_g, nn, cut, final_buffer, out, &kc, &nh);
   if (rc) return rc;
-  const int gk = grid_for(k, 256), gn = grid_for(n, 256);
-  k_stream_blocks<<<gk, 256, 0, st>>>(s->d_cluster_of, s->d_feats, k, cut, s->cfg.dt_max_ticks, final_buffer ? 1 : 0,
-                                      s->d_flag, s->d_size);
-  TPX_LAUNCHED(c);
-  if ((rc = exclusive_scan(c, s->d_flag, k, s->d_cidx, s->d_partials, s->d_counts + 0, st))) return rc;
-  if ((rc = exclusive_scan(c, s->d_size, k, s->d_hoff, s->d_partials, s->d_counts + 1, st))) return rc;
-  TPX_CUDA(cudaMemsetAsync(s->d_open, 0, n * 4, st));
-  stream_emit_args a;
-  a.hits = hits;
-  a.gidx = gidx;
-  a.order = s->d_order;
-  a.offsets = s->d_offsets;
-  a.cluster_of = s->d_cluster_of;
-  a.feats = s->d_feats;
-  a.closed_flag = s->d_flag;
-  a.cidx = s->d_cidx;
-  a.hoff = s->d_hoff;
-  a.k = k;
-  a.out_cl = s->d_out_cl;
-  a.out_hits = s->d_out_hits;
-  a.out_g = s->d_out_g;
-  a.open_flag = s->d_open;
-  k_stream_emit_small<<<gk, 256, 0, st>>>(a);
-  TPX_LAUNCHED(c);
-  k_stream_emit_large<<<gk, 256, 0, st>>>(a);
-  TPX_LAUNCHED(c);
-  if ((rc = exclusive_scan(c, s->d_open, n, s->d_cpos, s->d_partials, s->d_counts + 2, st))) return rc;
-  k_stream_carry<<<gn, 256, 0, st>>>(hits, gidx, n, s->d_open, s->d_cpos, s->d_carry, s->d_carry_g);
-  TPX_LAUNCHED(c);
-  TPX_CUDA(cudaMemcpyAsync(s->h_counts, s->d_counts, 12, cudaMemcpyDeviceToHost, st));
-  TPX_CUDA(cudaStreamSynchronize(st));
-  const uint64_t kc = s->h_counts[0], nh = s->h_counts[1], ncarry = s->h_counts[2];
   // batch of closed clusters (pinned, from the pool)
   stream_batch_store* b = nullptr;
   if (!s->pool.empty()) {
@@ -395,12 +475,11 @@ static int stream_process(tpx_stream* s, uint64_t cut, bool final_buffer) {
   b->hits.n = nh;
   b->g.n = nh;
   s->ready.push_back(b);
-  s->n_carry = ncarry;
   s->st.buffers++;
   s->st.clusters_out += kc;
   s->st.hits_out += nh;
-  s->st.carried_last = ncarry;
-  if (ncarry > s->st.carried_max) s->st.carried_max = ncarry;
+  s->st.carried_last = s->dev.n_carry;
+  if (s->dev.n_carry > s->st.carried_max) s->st.carried_max = s->dev.n_carry;
   s->st.device_ms += ms;
   return TPX_OK;
 }
@@ -422,14 +501,14 @@ int tpx_stream_workspace_bytes(const tpx_stream_config* cfg, size_t* bytes) {
 
 void tpx_stream_destroy(tpx_stream* s) {
   if (!s) return;
-  if (s->s) cudaStreamSynchronize(s->s);
+  if (s->dev.s) cudaStreamSynchronize(s->dev.s);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
-  if (s->h_counts) cudaFreeHost(s->h_counts);
+  if (s->dev.h_counts) cudaFreeHost(s->dev.h_counts);
   for (auto* b : s->ready) delete b;
   for (auto* b : s->pool) delete b;
   delete s->current;
-  tpx_cluster_destroy(s->ctx);
+  tpx_cluster_destroy(s->dev.ctx);
   delete s;
 }
 
@@ -445,12 +524,14 @@ int tpx_stream_create(const tpx_stream_config* cfg, void* workspace, size_t work
   if (!s) return TPX_ERR_OOM;
   memset(&s->st, 0, sizeof(s->st));
   s->cfg = *cfg;
-  rc = tpx_cluster_create(cfg->dt_max_ticks, TPX_VARIANT_LOCAL, cfg->width, cfg->height, &s->ctx);
+  rc = tpx_cluster_create(cfg->dt_max_ticks, TPX_VARIANT_LOCAL, cfg->width, cfg->height, &s->dev.ctx);
   if (rc) {
     delete s;
     return rc;
   }
-  s->s = (cudaStream_t)cuda_stream;
+  s->dev.s = (cudaStream_t)cuda_stream;
+  s->dev.cap = cfg->max_device_hits;
+  s->dev.dt = cfg->dt_max_ticks;
   s->bf.b = cfg->buffer_hits;
   s->bf.b_t = cfg->reserve_hits;
   s->bf.t = cfg->disorder_ticks;
@@ -458,35 +539,14 @@ int tpx_stream_create(const tpx_stream_config* cfg, void* workspace, size_t work
   tpx::stream_layout L;
   tpx::stream_layout_of(cfg, &L);
   char* w = (char*)workspace;
-  s->ws = w;
-  s->ws_bytes = workspace_bytes;
-  s->cap = cfg->max_device_hits;
   s->d_new = (tpx_hit*)(w + L.new_h);
   s->d_new_g = (uint64_t*)(w + L.new_g);
-  s->d_hits = (tpx_hit*)(w + L.hits);
-  s->d_g = (uint64_t*)(w + L.g);
-  s->d_carry = (tpx_hit*)(w + L.carry);
-  s->d_carry_g = (uint64_t*)(w + L.carry_g);
   s->d_out_hits = (tpx_hit*)(w + L.out_hits);
   s->d_out_g = (uint64_t*)(w + L.out_g);
-  s->d_labels = (uint32_t*)(w + L.labels);
-  s->d_order = (uint32_t*)(w + L.order);
-  s->d_offsets = (uint32_t*)(w + L.offsets);
-  s->d_cluster_of = (uint32_t*)(w + L.cluster_of);
-  s->d_flag = (uint32_t*)(w + L.flag);
-  s->d_size = (uint32_t*)(w + L.size);
-  s->d_cidx = (uint32_t*)(w + L.cidx);
-  s->d_hoff = (uint32_t*)(w + L.hoff);
-  s->d_open = (uint32_t*)(w + L.open);
-  s->d_cpos = (uint32_t*)(w + L.cpos);
-  s->d_counts = (uint32_t*)(w + L.counts);
-  s->d_partials = (uint32_t*)(w + L.partials);
-  s->d_feats = (tpx_cluster_features*)(w + L.feats);
   s->d_out_cl = (tpx_stream_cluster*)(w + L.out_cl);
-  s->d_run_ws = w + L.run_ws;
-  s->run_ws_bytes = workspace_bytes - L.run_ws;
+  tpx::stream_dev_bind(&s->dev, w, L.dev, workspace_bytes);
   if (cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess ||
-      cudaMallocHost(&s->h_counts, 64) != cudaSuccess || !s->bf.buf.reserve(1024) || !s->bf.next.reserve(1024) ||
+      cudaMallocHost(&s->dev.h_counts, 64) != cudaSuccess || !s->bf.buf.reserve(1024) || !s->bf.next.reserve(1024) ||
       !s->bf.buf_g.reserve(1024) || !s->bf.next_g.reserve(1024)) {
     tpx_stream_destroy(s);
     return TPX_ERR_CUDA;
@@ -552,7 +612,7 @@ int tpx_stream_pop(tpx_stream* s, tpx_stream_batch* out) {
 int tpx_stream_get_stats(const tpx_stream* s, tpx_stream_stats* out) {
   if (!s || !out) return TPX_ERR_INVALID_ARG;
   *out = s->st;
-  out->carried_last = s->n_carry;
+  out->carried_last = s->dev.n_carry;
   return TPX_OK;
 }
 
@@ -588,3 +648,5 @@ int tpx_buffill_assign(const tpx_hit* hits, uint64_t n, uint64_t b, uint64_t b_t
 }
 
 }  // extern "C"
+
+#include "stream_host.cuh"

@@ -117,3 +117,54 @@ def test_stream_capacity_error(tpx):
         s.push(h)
     assert e.value.status == -5
     s.close()
+
+
+# --------------------------------------------- one-shot host-to-host run
+def _run_host(tpx, h, dt, b, b_t, t_closing, max_dev=None, capacity=None, W=256, H=256):
+    r = tpx.StreamRunner(dt, b, b_t, _disorder(h), t_closing, max_device_hits=max_dev, width=W, height=H)
+    hh = torch.from_numpy(np.ascontiguousarray(h).view(np.uint8)).pin_memory()
+    order = np.zeros(max(len(h), 1), dtype=np.uint32)
+    cl = np.zeros(max(capacity or len(h), 1), dtype=tpx.STREAM_CLUSTER_DTYPE)
+    k = r.run(hh, order, cl, capacity=capacity or len(h))
+    return order[:len(h)], cl[:k], r.last_stats
+
+
+@pytest.mark.parametrize("b,b_t,t_closing", [(50_000, 10_000, 64), (20_000, 15_000, 0), (1_000_000, 30_000, 640)])
+def test_run_host_equals_push_api(tpx, b, b_t, t_closing):
+    h = tpxgen.generate("mixed", n_hits=600_000)
+    batches, _ = _check_stream(tpx, h, 320, b, b_t, t_closing)
+    order, cl, st = _run_host(tpx, h, 320, b, b_t, t_closing)
+    ref_order = np.concatenate([bt["hit_index"] for bt in batches]).astype(np.uint32)
+    assert np.array_equal(order, ref_order)
+    ref_cl = np.concatenate([bt["clusters"] for bt in batches])
+    for name in ("label", "size", "toa_min", "toa_max", "tot_sum", "sum_x", "sum_y", "sum_tot_x", "sum_tot_y"):
+        assert np.array_equal(cl[name], ref_cl[name]), name
+    # offsets index order_out; every block holds its cluster's hits
+    assert (np.diff(cl["offset"].astype(np.int64)) > 0).all() and int(cl["offset"][0]) == 0
+    assert st["hits_out"] == len(h) and st["late_hits"] == 0 and st["buffers"] == len(batches)
+
+
+def test_run_host_vs_oracle_presets(tpx):
+    for preset, dt, b, b_t, tc in (("heavyion", 64, 100_000, 20_000, 256), ("lowflux", 128, 40_000, 5_000, 64),
+                                   ("tiny", 128, 3_000, 1_000, 0)):
+        h = tpxgen.generate(preset, n_hits=None if preset == "tiny" else 300_000)
+        order, cl, st = _run_host(tpx, h, dt, b, b_t, tc, max_dev=4 * (b + b_t))
+        rl, rf = oracle.cluster(h, dt)
+        labels = np.empty(len(h), dtype=np.uint64)
+        for c in cl:
+            o, sz = int(c["offset"]), int(c["size"])
+            labels[order[o:o + sz]] = c["label"]
+        assert np.array_equal(labels.astype(np.uint32), rl), preset
+        srt = cl[np.argsort(cl["label"], kind="stable")]
+        assert np.array_equal(srt["label"], rf["label"].astype(np.uint64))
+        for name in ("size", "toa_min", "toa_max", "tot_sum", "sum_x", "sum_y", "sum_tot_x", "sum_tot_y"):
+            assert np.array_equal(srt[name].astype(np.uint64), rf[name].astype(np.uint64)), (preset, name)
+
+
+def test_run_host_capacity_and_empty(tpx):
+    h = tpxgen.generate("mixed", n_hits=100_000)
+    with pytest.raises(tpx.TpxError) as e:
+        _run_host(tpx, h, 320, 20_000, 5_000, 64, capacity=10)
+    assert e.value.status == -5
+    order, cl, st = _run_host(tpx, h[:0], 320, 20_000, 5_000, 64)
+    assert len(cl) == 0
