@@ -255,6 +255,30 @@ def run_ours(args):
         torch.cuda.synchronize()
     c.set_profiling(False)
     ms = ev0.elapsed_time(ev1) / args.steps
+    # ---- Step-6 grouped output + shape records (tpx_cluster_run_grouped, f3),
+    # same input, device-timed
+    grouped = None
+    if not args.no_grouped:
+        gout = {"labels": labels, "features": feats,
+                "shapes": torch.empty((n, 32), dtype=torch.uint8, device=dev),
+                "order": torch.empty(n, dtype=torch.int32, device=dev),
+                "offsets": torch.empty(n + 1, dtype=torch.int32, device=dev),
+                "cluster_of": torch.empty(n, dtype=torch.int32, device=dev)}
+        for _ in range(2):
+            c.run_grouped(d_hits, n=n, out=gout, workspace=wsbuf, stream=stream)
+        gsteps = max(2, min(args.steps, 5))
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(gsteps):
+            c.run_grouped(d_hits, n=n, out=gout, workspace=wsbuf, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        gms = ev0.elapsed_time(ev1) / gsteps
+        grouped = {"value": round(n / (gms * 1e-3) / 1e6, 2), "unit": "Mhit/s", "ms_per_step": round(gms, 4),
+                   "api": "tpx_cluster_run_grouped (run + Step-6 order + shape records)", "steps": gsteps,
+                   "grouping_ms": round(gms - ms, 4)}
+        del gout
+        torch.cuda.empty_cache()
     value = n / (ms * 1e-3) / 1e6  # Mhit/s
     clocks = clk.summary()
 
@@ -321,6 +345,7 @@ def run_ours(args):
                 "api": "tpx_pipeline_submit/wait (depth 3: copies of one buffer overlap the kernels of the others)",
                 "steps": e2e_steps},
         "e2e_stream": stream_e2e,
+        "grouped": grouped,
         "gpu_launches": launches,
         "roofline": roof,
         "hbm_alg_gbs_whole_path": round(whole_path_gbs, 2),
@@ -468,6 +493,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer legs (profiling runs only)")
     ap.add_argument("--no-stream", action="store_true", help="skip the streaming host-to-host leg")
+    ap.add_argument("--no-grouped", action="store_true", help="skip the grouped-output leg")
     ap.add_argument("--stream-buffer", type=int, default=10_000_000, help="BufFill buffer size b (hits)")
     args = ap.parse_args()
     if args.impl == "reference":

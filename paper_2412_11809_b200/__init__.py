@@ -237,12 +237,14 @@ class Clusterer:
         kk = min(k.value, capacity)
         return labels[:n], features[:kk], k.value
 
-    def run_grouped(self, hits, n: int | None = None, shapes: bool = True, stream=None):
+    def run_grouped(self, hits, n: int | None = None, shapes: bool = True, stream=None, out: dict | None = None,
+                    workspace=None):
         """``tpx_cluster_run_grouped``: labels, features, optional shape records
         and the cluster-contiguous order (Alg. GPU Step 6).
 
         Returns ``(labels, features, shapes|None, order, offsets, cluster_of, k)``
-        (device tensors; offsets has k + 1 entries).
+        (device tensors; offsets has k + 1 entries).  ``out`` may hold
+        preallocated tensors under those names (capacity n).
         """
         torch = _torch()
         assert hits.is_cuda and hits.is_contiguous()
@@ -250,18 +252,32 @@ class Clusterer:
             n = hits.numel() * hits.element_size() // 16
         dev = hits.device
         cap = max(n, 1)
-        labels = torch.empty(cap, dtype=torch.int32, device=dev)
-        features = torch.empty((cap, 64), dtype=torch.uint8, device=dev)
-        shp = torch.empty((cap, 32), dtype=torch.uint8, device=dev) if shapes else None
-        order = torch.empty(cap, dtype=torch.int32, device=dev)
-        offsets = torch.empty(cap + 1, dtype=torch.int32, device=dev)
-        cluster_of = torch.empty(cap, dtype=torch.int32, device=dev)
-        workspace = self._workspace(self.workspace_bytes(n), dev)
+        o = out or {}
+        labels = o.get("labels", None)
+        if labels is None:
+            labels = torch.empty(cap, dtype=torch.int32, device=dev)
+        features = o.get("features", None)
+        if features is None:
+            features = torch.empty((cap, 64), dtype=torch.uint8, device=dev)
+        shp = o.get("shapes", None)
+        if shp is None and shapes:
+            shp = torch.empty((cap, 32), dtype=torch.uint8, device=dev)
+        order = o.get("order", None)
+        if order is None:
+            order = torch.empty(cap, dtype=torch.int32, device=dev)
+        offsets = o.get("offsets", None)
+        if offsets is None:
+            offsets = torch.empty(cap + 1, dtype=torch.int32, device=dev)
+        cluster_of = o.get("cluster_of", None)
+        if cluster_of is None:
+            cluster_of = torch.empty(cap, dtype=torch.int32, device=dev)
+        if workspace is None:
+            workspace = self._workspace(self.workspace_bytes(n), dev)
         k = _u64(0)
         rc = _run_grouped(self._h, hits.data_ptr(), int(n), labels.data_ptr(), features.data_ptr(),
                           shp.data_ptr() if shapes else None, int(cap), ctypes.byref(k), order.data_ptr(),
-                          offsets.data_ptr(), cluster_of.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                          _stream_handle(stream))
+                          offsets.data_ptr(), cluster_of.data_ptr(), workspace.data_ptr(),
+                          workspace.numel() * workspace.element_size(), _stream_handle(stream))
         _check(rc, "tpx_cluster_run_grouped")
         kk = k.value
         return (labels[:n], features[:kk], shp[:kk] if shapes else None, order[:n], offsets[: kk + 1],
