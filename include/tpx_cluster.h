@@ -64,8 +64,15 @@ typedef struct tpx_cluster_features {
   uint64_t sum_tot_y;
 } tpx_cluster_features;
 
-/* PAPER.md §2 (iii)(a) l.39, (iii)(b) l.40, (iii)(c) l.41.  Only LOCAL is
- * implemented on the GPU path; the others return TPX_ERR_UNSUPPORTED. */
+/* PAPER.md §2 (iii)(a) l.39, (iii)(b) l.40, (iii)(c) l.41.  LOCAL is the
+ * connected-component definition above.  GLOBAL and STATIC follow the
+ * streaming convention (R11, R21): hits in (toa, index) order; a
+ * hit joins every existing cluster that has a member on one of its 9
+ * neighbouring pixels and satisfies toa - cluster.maxToA <= dt_max (GLOBAL)
+ * or toa - cluster.minToA <= dt_max (STATIC); all joinable clusters merge.
+ * Labels and records are defined as for LOCAL.  GLOBAL/STATIC contexts need
+ * a larger workspace (tpx_cluster_workspace_bytes) and support neither
+ * run_partial with n_owned < n nor the stream API. */
 enum {
   TPX_VARIANT_LOCAL = 0,
   TPX_VARIANT_GLOBAL = 1,
@@ -75,7 +82,7 @@ enum {
 enum {
   TPX_OK = 0,
   TPX_ERR_INVALID_ARG = -1,   /* null pointer, bad size, bad variant value     */
-  TPX_ERR_UNSUPPORTED = -2,   /* variant != LOCAL                              */
+  TPX_ERR_UNSUPPORTED = -2,   /* operation not available for this variant      */
   TPX_ERR_COORD_RANGE = -3,   /* some hit has x >= width or y >= height, or
                                  toa >= 2^48; outputs are unspecified          */
   TPX_ERR_TOO_MANY_HITS = -4, /* n >= 2^32 - 1 (labels are u32)                */
@@ -99,7 +106,7 @@ const char* tpx_status_string(int status);
  * equal ToAs connect).  variant: TPX_VARIANT_*.  width/height: sensor size in
  * pixels, 1..32768 (256x256 Timepix3, 448x512 Timepix4).  *out receives the
  * context (host memory owned by the library, freed by tpx_cluster_destroy).
- * Errors: INVALID_ARG, UNSUPPORTED (variant != LOCAL), CUDA. */
+ * Errors: INVALID_ARG, CUDA. */
 int tpx_cluster_create(uint64_t dt_max_ticks, int variant, uint32_t width,
                        uint32_t height, tpx_cluster** out);
 

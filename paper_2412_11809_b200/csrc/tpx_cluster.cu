@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "finalize.cuh"
 #include "group.cuh"
+#include "variant.cuh"
 #include "scan.cuh"
 #include "shard.cuh"
 #include "sort.cuh"
@@ -95,6 +96,8 @@ struct tpx_cluster {
   cudaEvent_t ev[kMaxStages + 1];
   tpx_run_stats stats;
   int cuda_ready;  // CUDA resources are created lazily by the first run
+  tpx_cluster* island;  // variants (b)/(c): (a)-context whose components are the islands
+  uint64_t island_dt;
 };
 
 #define TPX_CUDA(call)                                                                 \
@@ -363,6 +366,145 @@ static int cluster_global(tpx_cluster* c, const run_ptrs& r) {
   return TPX_OK;
 }
 
+// ---------------------------------------------------------------- variants
+// (iii)(b) GLOBAL / (iii)(c) STATIC (variant.cuh): islands from an (a)-run
+// with window W, the streaming process simulated per island, records by
+// label.  Workspace: the island run's own, then the arrays below.
+struct variant_layout {
+  size_t labels, feats, order, offsets, cluster_of, par, cmin, cmax, stamp, root_of, minidx, rbits, rbase, misc,
+      total;
+};
+
+static variant_layout make_variant_layout(uint64_t n) {
+  variant_layout V;
+  size_t off = make_layout(n).total;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const uint64_t nwords = (n + 31) / 32;
+  V.labels = take(n * 4);
+  V.feats = take(n * 64);
+  V.order = take(n * 4);
+  V.offsets = take(n * 4 + 4);
+  V.cluster_of = take(n * 4);
+  V.par = take(n * 4);
+  V.cmin = take(n * 8);
+  V.cmax = take(n * 8);
+  V.stamp = take(n * 4);
+  V.root_of = take(n * 4);
+  V.minidx = take(n * 4);
+  V.rbits = take(nwords * 4);
+  V.rbase = take(nwords * 4);
+  V.misc = take(256);
+  V.total = off;
+  return V;
+}
+
+static size_t run_ws_total(const tpx_cluster* c, uint64_t n) {
+  return c->variant == TPX_VARIANT_LOCAL ? make_layout(n).total : make_variant_layout(n).total;
+}
+
+__global__ void k_fill_iota32(uint32_t* __restrict__ a, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+
+static int run_variant(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* labels_out,
+                       tpx_cluster_features* features_out, uint64_t capacity, uint64_t* n_clusters_out, char* ws,
+                       size_t ws_bytes, cudaStream_t s) {
+  const variant_layout V = make_variant_layout(n);
+  uint32_t* order = (uint32_t*)(ws + V.order);
+  uint32_t* offsets = (uint32_t*)(ws + V.offsets);
+  uint32_t* par = (uint32_t*)(ws + V.par);
+  unsigned long long* cmin = (unsigned long long*)(ws + V.cmin);
+  unsigned long long* cmax = (unsigned long long*)(ws + V.cmax);
+  uint32_t* stamp = (uint32_t*)(ws + V.stamp);
+  uint32_t* root_of = (uint32_t*)(ws + V.root_of);
+  uint32_t* minidx = (uint32_t*)(ws + V.minidx);
+  uint32_t* rbits = (uint32_t*)(ws + V.rbits);
+  uint32_t* rbase = (uint32_t*)(ws + V.rbase);
+  unsigned long long* d_span = (unsigned long long*)(ws + V.misc);
+  uint32_t* partials = (uint32_t*)(ws + make_layout(n).partials);
+  const uint64_t dt = c->dt;
+  // (c): W = dt is exact; (b): start at 4 dt and grow until the span test holds
+  uint64_t W = c->variant == TPX_VARIANT_STATIC ? dt : 4 * dt + 64;
+  int rc;
+  for (int round = 0;; ++round) {
+    if (!c->island || c->island_dt != W) {
+      tpx_cluster_destroy(c->island);
+      c->island = nullptr;
+      if ((rc = tpx_cluster_create(W, TPX_VARIANT_LOCAL, c->width, c->height, &c->island))) return rc;
+      c->island_dt = W;
+    }
+    uint64_t k_is = 0;
+    rc = tpx_cluster_run_grouped(c->island, hits, n, (uint32_t*)(ws + V.labels), (tpx_cluster_features*)(ws + V.feats),
+                                 nullptr, n, &k_is, order, offsets, (uint32_t*)(ws + V.cluster_of), ws,
+                                 make_layout(n).total, s);
+    if (rc) return rc;
+    c->stats.kernel_launches += c->island->stats.kernel_launches;
+    const int gn = grid_for(n, 256), gk = grid_for(k_is, 256);
+    k_fill_iota32<<<gn, 256, 0, s>>>(par, n);
+    TPX_LAUNCHED(c);
+    TPX_CUDA(cudaMemsetAsync(stamp, 0, n * 4, s));
+    variant_args a;
+    a.hits = hits;
+    a.order = order;
+    a.offsets = offsets;
+    a.k = k_is;
+    a.dt = dt;
+    a.window = W;
+    a.rule = c->variant;
+    a.par = par;
+    a.cmin = cmin;
+    a.cmax = cmax;
+    a.stamp = stamp;
+    k_variant_small<<<gk, 256, 0, s>>>(a);
+    TPX_LAUNCHED(c);
+    k_variant_large<<<gk, 256, 0, s>>>(a);
+    TPX_LAUNCHED(c);
+    TPX_CUDA(cudaMemsetAsync(minidx, 0xff, n * 4, s));
+    TPX_CUDA(cudaMemsetAsync(d_span, 0, 8, s));
+    k_variant_roots<<<gn, 256, 0, s>>>(par, order, n, cmin, cmax, root_of, minidx, d_span);
+    TPX_LAUNCHED(c);
+    if (c->variant == TPX_VARIANT_GLOBAL) {
+      unsigned long long span = 0;
+      TPX_CUDA(cudaMemcpyAsync(&span, d_span, 8, cudaMemcpyDeviceToHost, s));
+      TPX_CUDA(cudaStreamSynchronize(s));
+      if (span + dt > W) {  // a candidate older than W might have been missed
+        const uint64_t grow = 2 * (span + dt) + 64;
+        W = grow > 4 * W ? grow : 4 * W;
+        c->stats.sort_retries++;
+        continue;
+      }
+    }
+    break;
+  }
+  k_variant_labels<<<grid_for(n, 256), 256, 0, s>>>(root_of, order, n, minidx, labels_out);
+  TPX_LAUNCHED(c);
+  // records in ascending label order
+  const uint64_t nwords = (n + 31) / 32;
+  k_root_bits<<<grid_for(nwords, 256), 256, 0, s>>>(labels_out, n, rbits);
+  TPX_LAUNCHED(c);
+  k_popc<<<grid_for(nwords, 256), 256, 0, s>>>(rbits, nwords, rbase);
+  TPX_LAUNCHED(c);
+  if ((rc = exclusive_scan(c, rbase, nwords, rbase, partials, (uint32_t*)(ws + V.misc + 64), s))) return rc;
+  if (capacity) {
+    k_variant_feat_init<<<grid_for(n, 256), 256, 0, s>>>(n, rbits, rbase, features_out, capacity);
+    TPX_LAUNCHED(c);
+    k_variant_feat_accum<<<grid_for(n, 256), 256, 0, s>>>(hits, n, labels_out, rbits, rbase, features_out, capacity);
+    TPX_LAUNCHED(c);
+  }
+  uint32_t k = 0;
+  TPX_CUDA(cudaMemcpyAsync(&k, ws + V.misc + 64, 4, cudaMemcpyDeviceToHost, s));
+  TPX_CUDA(cudaStreamSynchronize(s));
+  *n_clusters_out = k;
+  c->stats.n_clusters = k;
+  c->stats.cross_pairs = W;  // diagnostics: final island window (ticks)
+  return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
+}
+
 extern "C" {
 
 int tpx_abi_version(void) { return TPX_ABI_VERSION; }
@@ -371,7 +513,7 @@ const char* tpx_status_string(int s) {
   switch (s) {
     case TPX_OK: return "ok";
     case TPX_ERR_INVALID_ARG: return "invalid argument";
-    case TPX_ERR_UNSUPPORTED: return "unsupported (only variant (iii)(a) LOCAL runs on the GPU)";
+    case TPX_ERR_UNSUPPORTED: return "unsupported for this variant (sharded runs and streams: variant (iii)(a) only)";
     case TPX_ERR_COORD_RANGE: return "hit coordinate outside the sensor or toa >= 2^48";
     case TPX_ERR_TOO_MANY_HITS: return "too many hits (n must be < 2^32 - 1)";
     case TPX_ERR_CAPACITY: return "feature capacity too small (n_clusters_out holds the required count)";
@@ -390,7 +532,6 @@ int tpx_cluster_create(uint64_t dt_max_ticks, int variant, uint32_t width, uint3
   if (variant < TPX_VARIANT_LOCAL || variant > TPX_VARIANT_STATIC) return TPX_ERR_INVALID_ARG;
   if (width == 0 || height == 0 || width > 32768 || height > 32768) return TPX_ERR_INVALID_ARG;
   if (dt_max_ticks >= (1ull << 48)) return TPX_ERR_INVALID_ARG;
-  if (variant != TPX_VARIANT_LOCAL) return TPX_ERR_UNSUPPORTED;
   tpx_cluster* c = new (std::nothrow) tpx_cluster;
   if (!c) return TPX_ERR_OOM;
   memset(c, 0, sizeof(*c));
@@ -404,6 +545,7 @@ int tpx_cluster_create(uint64_t dt_max_ticks, int variant, uint32_t width, uint3
 
 void tpx_cluster_destroy(tpx_cluster* c) {
   if (!c) return;
+  tpx_cluster_destroy(c->island);
   if (c->cuda_ready) {
     for (int i = 0; i <= kMaxStages; ++i) cudaEventDestroy(c->ev[i]);
     cudaFreeHost(c->host_hdr);
@@ -414,7 +556,7 @@ void tpx_cluster_destroy(tpx_cluster* c) {
 int tpx_cluster_workspace_bytes(const tpx_cluster* c, uint64_t n, size_t* bytes) {
   if (!c || !bytes) return TPX_ERR_INVALID_ARG;
   if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
-  *bytes = make_layout(n).total;
+  *bytes = run_ws_total(c, n);
   return TPX_OK;
 }
 
@@ -458,6 +600,13 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   if (((uintptr_t)hits & 15) || ((uintptr_t)workspace & 255) || ((uintptr_t)features_out & 15) ||
       ((uintptr_t)labels_out & 3))
     return TPX_ERR_INVALID_ARG;
+  if (c->variant != TPX_VARIANT_LOCAL) {
+    if (n_owned != n) return TPX_ERR_UNSUPPORTED;  // sharded runs: variant (a) only
+    if (workspace_bytes < run_ws_total(c, n)) return TPX_ERR_OOM;
+    if (ensure_cuda(c)) return TPX_ERR_CUDA;
+    return run_variant(c, hits, n, labels_out, features_out, capacity, n_clusters_out, (char*)workspace,
+                       workspace_bytes, (cudaStream_t)stream);
+  }
   run_ptrs r;
   r.L = make_layout(n);
   if (workspace_bytes < r.L.total) return TPX_ERR_OOM;
@@ -653,7 +802,7 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
 int tpx_cluster_host_workspace_bytes(const tpx_cluster* c, uint64_t n, uint64_t capacity, size_t* bytes) {
   if (!c || !bytes) return TPX_ERR_INVALID_ARG;
   if (n >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
-  *bytes = align256(n * 16) + align256(n * 4) + align256(capacity * 64) + make_layout(n).total;
+  *bytes = align256(n * 16) + align256(n * 4) + align256(capacity * 64) + run_ws_total(c, n);
   return TPX_OK;
 }
 

@@ -65,7 +65,11 @@ def test_create_validates_without_gpu(lib):
     assert c.workspace_bytes(0) >= 256
     assert c.workspace_bytes(10**6) > 16 * 10**6
     c.close()
-    for kw, code in ((dict(variant=1), -2), (dict(variant=2), -2), (dict(variant=7), -1),
+    for v in (1, 2):  # variants (iii)(b)/(c) are supported; their workspace is larger
+        cv = lib.Clusterer(128, variant=v)
+        assert cv.workspace_bytes(10**6) > lib.Clusterer(128).workspace_bytes(10**6)
+        cv.close()
+    for kw, code in ((dict(variant=7), -1), (dict(variant=-1), -1),
                      (dict(width=0), -1), (dict(height=70000), -1)):
         with pytest.raises(lib.TpxError) as e:
             lib.Clusterer(128, **kw)

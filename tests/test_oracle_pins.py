@@ -321,3 +321,31 @@ def test_group_empty():
     order, offsets, cof = oracle.group(h, labels, feats)
     assert len(order) == 0 and offsets.tolist() == [0] and len(cof) == 0
     assert len(oracle.shapes(h, labels, feats)) == 0
+
+
+# --------------------------- streaming variants (iii)(b)/(c): structural pins
+def test_streaming_variant_invariants():
+    """(c) STATIC: every join is within dt of the cluster's
+    first hit, so each (c)-cluster spans <= dt and is connected by (a)-edges
+    -> (c) refines (a).  (b) GLOBAL (l.40): every (a)-edge is a (b)-join, so
+    (a) refines (b), and each (b)-cluster's sorted ToAs have gaps <= dt
+    (R21).  LOCAL streaming equals the CC oracle."""
+    rng = np.random.default_rng(31)
+    for trial in range(80):
+        W, H = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        dt = int(rng.choice([0, 2, 5, 16]))
+        h = tpxgen.random_small(rng, int(rng.integers(1, 250)), W, H, max(6 * dt, 4))
+        la, _ = oracle.cluster(h, dt, W, H)
+        lb = oracle.cluster_streaming(h, dt, oracle.GLOBAL, W, H)
+        lc = oracle.cluster_streaming(h, dt, oracle.STATIC, W, H)
+        assert np.array_equal(oracle.cluster_streaming(h, dt, oracle.LOCAL, W, H), la)
+        assert pins.is_refinement(lc, la) and pins.is_refinement(la, lb), trial
+        toa = h["toa"].astype(np.int64)
+        for lab in np.unique(lc):
+            t = toa[lc == lab]
+            assert t.max() - t.min() <= dt
+        for lab in np.unique(lb):
+            t = np.sort(toa[lb == lab])
+            assert (np.diff(t) <= dt).all()
+        for lab_arr in (lb, lc):  # canonical labels
+            assert (lab_arr <= np.arange(len(h))).all() and np.array_equal(lab_arr[lab_arr], lab_arr)
