@@ -279,6 +279,32 @@ def run_ours(args):
                    "grouping_ms": round(gms - ms, 4)}
         del gout
         torch.cuda.empty_cache()
+    # ---- variants (iii)(b) global / (iii)(c) static (f2) on the first 50M hits
+    # of the same stream, device-timed
+    variants = None
+    if not args.no_variants:
+        variants = {}
+        nv = min(n, 50_000_000)
+        for vname, vid in (("global", 1), ("static", 2)):
+            cv = tpx.Clusterer(dt, variant=vid)
+            vws = torch.empty(cv.workspace_bytes(nv), dtype=torch.uint8, device=dev)
+            vlab = torch.empty(nv, dtype=torch.int32, device=dev)
+            vft = torch.empty((nv, 64), dtype=torch.uint8, device=dev)
+            cv.run(d_hits, n=nv, labels=vlab, features=vft, capacity=nv, workspace=vws, stream=stream)
+            vsteps = 3
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for _ in range(vsteps):
+                _, _, kv = cv.run(d_hits, n=nv, labels=vlab, features=vft, capacity=nv, workspace=vws, stream=stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            vms = ev0.elapsed_time(ev1) / vsteps
+            variants[vname] = {"value": round(nv / (vms * 1e-3) / 1e6, 2), "unit": "Mhit/s",
+                               "ms_per_step": round(vms, 3), "n_hits": nv, "n_clusters": int(kv),
+                               "island_window_ticks": int(cv.stats()["cross_pairs"])}
+            del vws, vlab, vft
+            cv.close()
+            torch.cuda.empty_cache()
     value = n / (ms * 1e-3) / 1e6  # Mhit/s
     clocks = clk.summary()
 
@@ -346,6 +372,7 @@ def run_ours(args):
                 "steps": e2e_steps},
         "e2e_stream": stream_e2e,
         "grouped": grouped,
+        "variants": variants,
         "gpu_launches": launches,
         "roofline": roof,
         "hbm_alg_gbs_whole_path": round(whole_path_gbs, 2),
@@ -494,6 +521,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer legs (profiling runs only)")
     ap.add_argument("--no-stream", action="store_true", help="skip the streaming host-to-host leg")
     ap.add_argument("--no-grouped", action="store_true", help="skip the grouped-output leg")
+    ap.add_argument("--no-variants", action="store_true", help="skip the (iii)(b)/(c) variant legs")
     ap.add_argument("--stream-buffer", type=int, default=10_000_000, help="BufFill buffer size b (hits)")
     args = ap.parse_args()
     if args.impl == "reference":
