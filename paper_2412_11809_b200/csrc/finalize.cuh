@@ -149,6 +149,7 @@ __global__ void k_popc(const uint32_t* __restrict__ bitmap, uint64_t nwords, uin
 constexpr int kEmitThreads = 256;
 __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_features* __restrict__ stage,
                                                        const uint32_t* __restrict__ comp_count, uint32_t n_tiles,
+                                                       uint32_t tile,
                                                        const uint32_t* __restrict__ bitmap,
                                                        const uint32_t* __restrict__ wbase,
                                                        tpx_cluster_features* __restrict__ out, uint64_t capacity) {
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
     const uint32_t cc = comp_count[t];
-    const uint4* src = reinterpret_cast<const uint4*>(stage + (uint64_t)t * kTile);
+    const uint4* src = reinterpret_cast<const uint4*>(stage + (uint64_t)t * tile);
     for (uint32_t q0 = 0; q0 < cc * 4; q0 += 32) {  // warp-uniform trip count
       const uint32_t q = q0 + lane;
       const bool valid = q < cc * 4;

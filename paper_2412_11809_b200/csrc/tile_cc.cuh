@@ -32,15 +32,14 @@
 
 namespace tpx {
 
-constexpr int kTileThreads = 256;
-constexpr int kTile = 1024;                    // tile hits per CTA
+constexpr int kTile = 1024;                    // smallest tile (comp_count sizing)
+constexpr int kMaxTile = 2048;                 // largest tile (stage slot sizing)
 constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
 constexpr uint32_t kPixEmpty = 0xfffffu;       // empty hash slot key (pixel ids must be < 2^20 - 1)
 constexpr uint32_t kMaxTilePixels = 0xfffffu;  // sensors with more pixels take the global path
 constexpr uint16_t kNil = 0xffffu;             // end of a pixel list
 constexpr int kBuckets = 1024;                 // sparse: one bucket per pixel column (wider sensors: global path)
 constexpr int kBucketCap = 512;                // sparse: longer buckets take the global path
-constexpr int kItemsPerThread = kTile / kTileThreads;      // 4
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and chunk
 
@@ -48,22 +47,26 @@ constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and 
 // the tile's last hit.  Sparse streams (windows of tens of hits) use a 1024
 // halo and fit 4 CTAs per SM; dense heavy-ion streams (windows of ~1-3k hits,
 // SURVEY H1) use a 3072 halo at 2 CTAs per SM so that windows stay on chip.
-template <int kHaloHits, int kMinBlocks, bool kHashIndex>
+template <int kTileHits, int kThreadsPerCta, int kHaloHits, int kMinBlocks, bool kHashIndex>
 struct tile_cfg {
+  static constexpr int kTile = kTileHits;                         // tile hits per CTA
+  static constexpr int kThreads = kThreadsPerCta;
+  static constexpr int kItems = kTileHits / kThreadsPerCta;       // tile hits per thread
   static constexpr int kHalo = kHaloHits;
   static constexpr int kFwdMax = kTile + kHaloHits;               // tile + forward halo (local index l)
-  static constexpr int kStageItems = kFwdMax / kTileThreads;
+  static constexpr int kStageItems = kFwdMax / kThreads;
   static constexpr bool kRegStage = kStageItems <= 8;             // stage in registers, else re-read S
   static constexpr int kBlocks = kMinBlocks;
   static constexpr bool kHash = kHashIndex;                       // pixel hash (dense) vs column buckets (sparse)
-  static constexpr int kSlotBits = kHaloHits > 1024 ? 13 : 12;   // pixel hash slots (load <= 1/2)
+  static constexpr int kSlotBits = kFwdMax <= 2048 ? 12 : 13;     // pixel hash slots (load <= 1/2)
   static constexpr int kSlots = 1 << kSlotBits;
-  static_assert(kFwdMax % kTileThreads == 0, "staging layout");
+  static_assert(kFwdMax % kThreads == 0 && kTile % kThreads == 0 && kTile % ::tpx::kTile == 0 &&
+                    kTile <= kMaxTile, "staging layout");
   static_assert(kFwdMax <= 4096, "12-bit list heads");
   static_assert(kSlots >= 2 * kFwdMax, "hash load");
 };
-using tile_sparse = tile_cfg<1024, 4, false>;
-using tile_dense = tile_cfg<3072, 2, true>;
+using tile_sparse = tile_cfg<1024, 256, 1024, 4, false>;
+using tile_dense = tile_cfg<2048, 512, 2048, 2, true>;
 
 struct tile_args {
   const srec* S;
@@ -183,10 +186,14 @@ __device__ __forceinline__ void set_label_bit(uint32_t* bitmap, uint32_t label) 
 template <class C>
 struct tile_smem_buckets {
   static constexpr size_t kFwdMax = C::kFwdMax;
+  static constexpr size_t kTile = C::kTile;
+  static constexpr size_t kTileThreads = C::kThreads;
   static constexpr size_t csort = 0;                                   // uint2 [kFwdMax] (toa - base, y<<16|x)
   static constexpr size_t ckey = csort + (size_t)kFwdMax * 8;           // u32   [kFwdMax] y<<16 | local index
   static constexpr size_t myrank = ckey + (size_t)kFwdMax * 4;          // u16   [kFwdMax]
-  static constexpr size_t region_a = myrank + (size_t)kFwdMax * 2;
+  static constexpr size_t region_a_index = myrank + (size_t)kFwdMax * 2;
+  static constexpr size_t region_a_reduce = (size_t)kTile * 24;
+  static constexpr size_t region_a = region_a_index > region_a_reduce ? region_a_index : region_a_reduce;
   // reduction-phase aliases of region A
   static constexpr size_t stile = 0;                                   // uint4 [kTile]
   static constexpr size_t mem = stile + (size_t)kTile * 16;             // u16   [kTile]
@@ -214,6 +221,8 @@ struct tile_smem_buckets {
 template <class C>
 struct tile_smem_hash {
   static constexpr size_t kFwdMax = C::kFwdMax;
+  static constexpr size_t kTile = C::kTile;
+  static constexpr size_t kTileThreads = C::kThreads;
   static constexpr size_t tab = 0;                                      // u32 [kSlots] pixel << 12 | list head
   static constexpr size_t stoa = tab + (size_t)C::kSlots * 4;           // u32 [kFwdMax] toa - base
   static constexpr size_t nxt = stoa + (size_t)kFwdMax * 4;             // u16 [kFwdMax] next in pixel list
@@ -247,6 +256,7 @@ constexpr size_t tile_smem_bytes() {
 constexpr uint32_t kBigComp = 24;  // components this large are reduced by a whole warp
 
 // Block-wide exclusive scan (kTileThreads threads) of one u32 per thread.
+template <int kTileThreads>
 __device__ __forceinline__ uint32_t tile_block_scan(uint32_t v, uint32_t* total, uint32_t* s_wsum) {
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -317,8 +327,11 @@ struct feat_acc {
 };
 
 template <class C>
-__global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args a) {
+__global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a) {
   using SL = tile_smem_layout<C>;
+  constexpr int kTile = C::kTile;
+  constexpr int kTileThreads = C::kThreads;
+  constexpr int kItemsPerThread = C::kItems;
   constexpr int kStageItems = C::kStageItems;
   extern __shared__ __align__(16) unsigned char sm[];
   // index arrays of the two configurations (only one set is used):
@@ -500,7 +513,7 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
       mx = __reduce_max_sync(kFull, mx);
       if (lane == 0) atomicMax(&s_bmax, mx);
       uint32_t tot;
-      uint32_t ex = tile_block_scan(s, &tot, s_wsum);
+      uint32_t ex = tile_block_scan<kTileThreads>(s, &tot, s_wsum);
   #pragma unroll
       for (int i = 0; i < PT; ++i) {
         bs[threadIdx.x * PT + i] = ex;
@@ -775,7 +788,7 @@ __global__ void __launch_bounds__(kTileThreads, C::kBlocks) k_tile_cc(tile_args 
       my += v;
     }
     uint32_t total;
-    uint32_t ex = tile_block_scan(my, &total, s_wsum);
+    uint32_t ex = tile_block_scan<kTileThreads>(my, &total, s_wsum);
 #pragma unroll
     for (int q = 0; q < kItemsPerThread; ++q) {
       const uint32_t j = threadIdx.x * kItemsPerThread + q;

@@ -62,7 +62,7 @@ layout make_layout(uint64_t n) {
   L.S = take(n * 16);
   L.parent = take(n * 4);
   L.slot_of = take(n * 4);
-  L.stage = take((size_t)L.tiles * kTile * 64);
+  L.stage = take((size_t)n_tiles_of(n, kMaxTile) * kMaxTile * 64);
   L.comp_count = take((size_t)L.tiles * 4);
   L.open_hits = take(n * 4);
   L.open_comps = take(n * 4);
@@ -294,9 +294,11 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.verify_stride = kWSortTile;
   a.phase_cycles = c->profiling >= 2 ? hdr->phase_cycles : nullptr;
   if (r.dense)
-    k_tile_cc<tile_dense><<<L.tiles, kTileThreads, tile_smem_bytes<tile_dense>(), r.s>>>(a);
+    k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
+                            r.s>>>(a);
   else
-    k_tile_cc<tile_sparse><<<L.tiles, kTileThreads, tile_smem_bytes<tile_sparse>(), r.s>>>(a);
+    k_tile_cc<tile_sparse><<<n_tiles_of(r.n, tile_sparse::kTile), tile_sparse::kThreads,
+                             tile_smem_bytes<tile_sparse>(), r.s>>>(a);
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[2], r.s);
@@ -318,7 +320,9 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   int rc = exclusive_scan(c, wcnt, L.nwords, wcnt, partials, (uint32_t*)&hdr->n_clusters, r.s);
   if (rc) return rc;
   if (r.capacity) {
-    k_emit<<<kListGrid, kEmitThreads, 0, r.s>>>(stage, comp_count, L.tiles, bitmap, wcnt, r.feats, r.capacity);
+    const uint32_t tile = r.dense ? tile_dense::kTile : tile_sparse::kTile;
+    k_emit<<<kListGrid, kEmitThreads, 0, r.s>>>(stage, comp_count, n_tiles_of(r.n, tile), tile, bitmap, wcnt, r.feats,
+                                                r.capacity);
     TPX_LAUNCHED(c);
   }
   if (c->profiling) cudaEventRecord(c->ev[4], r.s);
