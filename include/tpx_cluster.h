@@ -239,10 +239,12 @@ int tpx_cluster_last_stats(const tpx_cluster* ctx, tpx_run_stats* out);
 int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
 
 /* Tile configuration of the clustering kernel: TPX_TILE_AUTO (default) lets
- * a window-density probe on the sorted stream choose; TPX_TILE_SPARSE /
- * TPX_TILE_DENSE force one (results are identical; only speed differs --
- * used by the parity tests to cover both).  Errors: INVALID_ARG. */
-enum { TPX_TILE_AUTO = 0, TPX_TILE_SPARSE = 1, TPX_TILE_DENSE = 2 };
+ * a window-density probe on the sorted stream choose; TPX_TILE_SPARSE (2x2-pixel
+ * cell index, 2048-hit tiles) / TPX_TILE_DENSE (pixel hash, large halo) force
+ * one; TPX_TILE_COLUMN forces the earlier column-bucket sparse kernel (kept for
+ * comparison).  Results are identical; only speed differs -- the parity tests
+ * cover every mode.  Errors: INVALID_ARG. */
+enum { TPX_TILE_AUTO = 0, TPX_TILE_SPARSE = 1, TPX_TILE_DENSE = 2, TPX_TILE_COLUMN = 3 };
 int tpx_cluster_set_tile_mode(tpx_cluster* ctx, int mode);
 
 /* Static name of stage i (0 <= i < 16) as reported in stage_ms; "" if unused. */

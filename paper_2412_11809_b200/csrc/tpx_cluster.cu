@@ -18,6 +18,7 @@
 #include "cluster.cuh"
 #include "common.cuh"
 #include "finalize.cuh"
+#include "tile_cell.cuh"
 #include "group.cuh"
 #include "variant.cuh"
 #include "scan.cuh"
@@ -130,7 +131,9 @@ static int ensure_cuda(tpx_cluster* c) {
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_dense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tile_smem_bytes<tile_dense>()) != cudaSuccess)
+                           (int)tile_smem_bytes<tile_dense>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tile_cell<cell_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)cell_smem_bytes<cell_sparse>()) != cudaSuccess)
     return TPX_ERR_CUDA;
   if (cudaMallocHost(&c->host_hdr, sizeof(dev_hdr)) != cudaSuccess) return TPX_ERR_CUDA;
   for (int i = 0; i <= kMaxStages; ++i) {
@@ -212,7 +215,8 @@ struct run_ptrs {
   char* ws;
   layout L;
   cudaStream_t s;
-  bool dense;  // tile configuration chosen by the density probe
+  bool dense;   // tile configuration chosen by the density probe
+  bool column;  // legacy column-bucket sparse kernel (TPX_TILE_COLUMN, comparison only)
 };
 
 static int reset_header(tpx_cluster* c, const run_ptrs& r) {
@@ -296,9 +300,12 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   if (r.dense)
     k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
                             r.s>>>(a);
-  else
+  else if (r.column)
     k_tile_cc<tile_sparse><<<n_tiles_of(r.n, tile_sparse::kTile), tile_sparse::kThreads,
                              tile_smem_bytes<tile_sparse>(), r.s>>>(a);
+  else
+    k_tile_cell<cell_sparse><<<n_tiles_of(r.n, cell_sparse::kTile), cell_sparse::kThreads,
+                               cell_smem_bytes<cell_sparse>(), r.s>>>(a);
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[2], r.s);
@@ -320,7 +327,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   int rc = exclusive_scan(c, wcnt, L.nwords, wcnt, partials, (uint32_t*)&hdr->n_clusters, r.s);
   if (rc) return rc;
   if (r.capacity) {
-    const uint32_t tile = r.dense ? tile_dense::kTile : tile_sparse::kTile;
+    const uint32_t tile = r.dense ? tile_dense::kTile : r.column ? tile_sparse::kTile : cell_sparse::kTile;
     k_emit<<<kListGrid, kEmitThreads, 0, r.s>>>(stage, comp_count, n_tiles_of(r.n, tile), tile, bitmap, wcnt, r.feats,
                                                 r.capacity);
     TPX_LAUNCHED(c);
@@ -572,7 +579,7 @@ int tpx_cluster_set_profiling(tpx_cluster* c, int enable) {
 }
 
 int tpx_cluster_set_tile_mode(tpx_cluster* c, int mode) {
-  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_DENSE) return TPX_ERR_INVALID_ARG;
+  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_COLUMN) return TPX_ERR_INVALID_ARG;
   c->tile_mode = mode;
   return TPX_OK;
 }
@@ -668,6 +675,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       } else {
         r.dense = c->tile_mode == TPX_TILE_DENSE;
       }
+      r.column = c->tile_mode == TPX_TILE_COLUMN;
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
     c->stats.sort_retries = attempt < 2 ? attempt : 2;

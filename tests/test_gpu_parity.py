@@ -108,14 +108,43 @@ def test_presets(tpx, preset, n):
     _assert_parity(tpx, h, p["dt_max"], W, H, ctx=preset)
 
 
-@pytest.mark.parametrize("mode", ["sparse", "dense"])
-@pytest.mark.parametrize("preset,n", [("mixed", 1_000_000), ("heavyion", 1_000_000), ("lowflux", 500_000)])
+@pytest.mark.parametrize("mode", ["sparse", "dense", "column"])
+@pytest.mark.parametrize("preset,n", [("mixed", 1_000_000), ("heavyion", 1_000_000), ("lowflux", 500_000),
+                                      ("timepix4", 1_000_000)])
 def test_forced_tile_modes(tpx, mode, preset, n):
-    """Both tile configurations give the oracle's result on every workload
+    """Every tile configuration gives the oracle's result on every workload
     (the density probe only chooses the faster one)."""
     h = tpxgen.generate(preset, n_hits=n)
-    st = _assert_parity(tpx, h, tpxgen.PRESETS[preset]["dt_max"], ctx=f"{preset}/{mode}", tile_mode=mode)
+    W, H = (448, 512) if preset == "timepix4" else (256, 256)
+    st = _assert_parity(tpx, h, tpxgen.PRESETS[preset]["dt_max"], W, H, ctx=f"{preset}/{mode}", tile_mode=mode)
     assert st["tile_dense"] == (mode == "dense")
+
+
+@pytest.mark.parametrize("mode", ["sparse", "column"])
+def test_forced_sparse_small_and_fuzz(tpx, mode):
+    """Sparse kernels on small and odd sensors (cell aliasing: widths/heights
+    above 256 share cell slots modulo 256 pixels), tiny dt and ragged sizes."""
+    rng = np.random.default_rng(78)
+    for trial in range(40):
+        W, H = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        dt = int(rng.choice([0, 3, 128]))
+        h = tpxgen.random_small(rng, int(rng.integers(1, 5000)), W, H, max(4 * dt, 3))
+        _assert_parity(tpx, h, dt, W, H, ctx=f"{mode} trial {trial}", tile_mode=mode)
+    for trial in range(6):
+        W, H = int(rng.integers(250, 1025)), int(rng.integers(250, 1025))
+        dt = int(rng.choice([3, 64, 320]))
+        nc = int(rng.integers(100, 4000))
+        cx, cy = rng.integers(0, W, nc), rng.integers(0, H, nc)
+        ct = np.sort(rng.integers(0, 200 * dt, nc))
+        k = rng.integers(0, nc, 8 * nc)  # 8 hits per blob on average, clipped to the sensor
+        h = np.zeros(len(k), dtype=tpxgen.HIT_DTYPE)
+        h["x"] = np.clip(cx[k] + rng.integers(-2, 3, len(k)), 0, W - 1)
+        h["y"] = np.clip(cy[k] + rng.integers(-2, 3, len(k)), 0, H - 1)
+        h["toa"] = ct[k] + rng.integers(0, dt + 1, len(k))
+        h["tot"] = rng.integers(1, 1024, len(k))
+        _assert_parity(tpx, h, dt, W, H, ctx=f"{mode} wide-sensor trial {trial}", tile_mode=mode)
+    for n in (2047, 2048, 2049, 4097, 65537):
+        _assert_parity(tpx, tpxgen.generate("mixed", n_hits=n), 320, ctx=f"{mode} n={n}", tile_mode=mode)
 
 
 def test_forced_dense_small_and_fuzz(tpx):
