@@ -88,6 +88,7 @@ struct tile_args {
   dev_hdr* hdr;
   uint32_t verify_stride;    // sorted-tile size whose borders are verified
   unsigned long long* phase_cycles;  // optional per-phase clock totals (profiling), may be null
+  const uint64_t* tile_meta;  // k_tile_bounds output (k_tile_cell only)
 };
 
 #define TPX_PHASE(k)                                                         \

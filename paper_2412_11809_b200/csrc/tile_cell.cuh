@@ -22,12 +22,9 @@
 //    The first entry of each list is tested with predicated, unconditional
 //    loads; longer lists continue in one warp-uniform loop, so the warp stays
 //    converged (no per-lane re-execution of the code after the search).
-//  * unions: every edge (j, q), q > j, first hooks q under its smallest
-//    earlier neighbour (atomicMin, an ECL-CC style initial forest with
-//    parent < child) and goes to a CTA edge list; after a barrier the
-//    non-hook edges are united (lock-free CAS, larger root under smaller ->
-//    root = earliest hit, the paper's time-invariant l.219-221), balanced
-//    over all threads.
+//  * unions: each lane buffers its edges (j, q), q > j, and unites them
+//    after its chunk's search (lock-free CAS, larger root under smaller ->
+//    root = earliest hit, the paper's time-invariant l.219-221).
 //  * features: tile hits are mapped to lanes in local-index (= time) order;
 //    lanes with the same root form runs, a segmented warp scan sums each run
 //    and the run's last lane folds it into the component's shared-memory
@@ -85,11 +82,6 @@ struct cell_smem {
   static constexpr size_t hb = nxt + kM * 2;                           // uint2 [kBackCap]
   static constexpr size_t crank = hb + (size_t)kBackCap * 8;           // u16 [kT] stage rank by root
   static constexpr size_t aslot = crank + kT * 2;                      // u16 [kT] accumulator slot by root
-  // edge list (j << 16 | q) of the search phase: the part of region A the
-  // cell heads leave free (the accumulators are written only after the unions)
-  static constexpr size_t elist = heads_end;
-  static constexpr uint32_t kEdgeCap = (uint32_t)((region_a - heads_end) / 4);
-  static_assert(kEdgeCap >= 1024, "edge list capacity");
   static_assert(aslot == crank + kT * 2 && (size_t)kEdgeBuf * C::kThreads * 2 <= kT * 4,
                 "per-lane edge buffers alias crank + aslot");
   static constexpr size_t hflag = aslot + kT * 2;                      // u8 [kT] bit0 open mark, bit1 overflow
@@ -141,6 +133,51 @@ __device__ __forceinline__ void tile_run_wide(const tile_args& a, uint64_t t0, u
   if (threadIdx.x == 0) a.comp_count[blockIdx.x] = nt;
 }
 
+// Per-tile staging bounds, one warp per tile (run before k_tile_cell so the
+// tile kernel starts its loads at once instead of waiting for two dependent
+// binary searches): the 8-word record k_tile_cell keeps in s_meta --
+//   [0] b0 (back halo start)  [1] f1 (forward halo end)  [2] base ToA
+//   [3] back-truncated flag   [4] ToA of the first unstaged hit (if truncated)
+//   [5] ToA of the previous tile's last hit   [6] largest staged ToA
+//   [7] forward-truncated flag (2)
+// and the sort-order check at sorted-tile borders.
+template <class C>
+__global__ void __launch_bounds__(256) k_tile_bounds(const srec* __restrict__ S, uint64_t n, uint64_t dt,
+                                                     uint32_t n_tiles, uint32_t verify_stride,
+                                                     uint64_t* __restrict__ meta, dev_hdr* hdr) {
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = lane_id();
+  if (t >= n_tiles) return;
+  const uint64_t t0 = (uint64_t)t * C::kTile, t1 = min(n, t0 + C::kTile);
+  const uint64_t toa_first = srec_key_toa(S, t0), toa_last = srec_key_toa(S, t1 - 1);
+  const uint64_t blim = t0 > (uint64_t)kBackCap ? t0 - kBackCap : 0;
+  const uint64_t b0 = warp_lower_bound(blim, t0, [&](uint64_t p) { return srec_key_toa(S, p) + dt >= toa_first; });
+  const uint64_t flim = min(n, t1 + (uint64_t)C::kHalo);
+  const uint64_t f1 = warp_lower_bound(t1, flim, [&](uint64_t p) { return srec_key_toa(S, p) > toa_last + dt; });
+  uint64_t v = 0;
+  const bool btrunc = b0 == blim && blim > 0;
+  const bool ftrunc = f1 == flim && flim < n;
+  switch (lane) {
+    case 0: v = b0; break;
+    case 1: v = f1; break;
+    case 2: v = srec_key_toa(S, b0); break;
+    case 3: v = (btrunc && srec_key_toa(S, blim - 1) + dt >= toa_first) ? 1u : 0u; break;
+    case 4: v = (ftrunc && srec_key_toa(S, flim) <= toa_last + dt) ? srec_key_toa(S, f1) : 0; break;
+    case 5: v = t0 ? srec_key_toa(S, t0 - 1) : 0; break;
+    case 6: v = srec_key_toa(S, f1 - 1); break;
+    case 7: v = (ftrunc && srec_key_toa(S, flim) <= toa_last + dt) ? 2u : 0u; break;
+    case 8:
+      if (t0 > 0 && (t0 % verify_stride) == 0) {  // strictly increasing (toa, index)
+        const srec p = load_srec(S + t0 - 1), q = load_srec(S + t0);
+        const uint64_t tp = srec_toa(p), tq = srec_toa(q);
+        if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&hdr->sort_bad, 1u);
+      }
+      break;
+    default: break;
+  }
+  if (lane < 8) meta[(uint64_t)t * 8 + lane] = v;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args a) {
   using SL = cell_smem<C>;
@@ -168,13 +205,12 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   uint2* hb = reinterpret_cast<uint2*>(sp(SL::hb));
   uint16_t* crank = reinterpret_cast<uint16_t*>(sp(SL::crank));
   uint16_t* aslot = reinterpret_cast<uint16_t*>(sp(SL::aslot));
-  uint32_t* elist = reinterpret_cast<uint32_t*>(sp(SL::elist));
   uint8_t* hflag = reinterpret_cast<uint8_t*>(sp(SL::hflag));
   uint8_t* copen = reinterpret_cast<uint8_t*>(sp(SL::copen));
   uint8_t* multi = reinterpret_cast<uint8_t*>(sp(SL::multi));
   __shared__ uint64_t s_meta[8];
   __shared__ uint32_t s_wsum[kTh / 32];
-  __shared__ uint32_t s_chunk, s_ne;
+  __shared__ uint32_t s_chunk;
 
   const uint64_t n = a.n, dt = a.dt;
   const srec* __restrict__ S = a.S;
@@ -184,35 +220,17 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   long long t_phase = clock64();
 
-  // ---- halo ranges (warp 0: back halo, warp 1: forward halo), sort check
-  if (warp == 0) {
-    const uint64_t toa_first = srec_key_toa(S, t0);
-    const uint64_t blim = t0 > (uint64_t)kBackCap ? t0 - kBackCap : 0;
-    const uint64_t b0 = warp_lower_bound(blim, t0, [&](uint64_t p) { return srec_key_toa(S, p) + dt >= toa_first; });
-    if (lane == 0) {
-      const bool btrunc = b0 == blim && blim > 0 && srec_key_toa(S, blim - 1) + dt >= toa_first;
-      s_meta[0] = b0;
-      s_meta[2] = srec_key_toa(S, b0);               // base: the smallest staged ToA
-      s_meta[3] = btrunc ? 1u : 0u;
-      s_meta[5] = t0 ? srec_key_toa(S, t0 - 1) : 0;  // ToA of the previous tile's last hit
-      s_chunk = 0;
-      s_ne = 0;
-    }
-  } else if (warp == 1) {
-    const uint64_t toa_last = srec_key_toa(S, t1 - 1);
-    const uint64_t flim = min(n, t1 + (uint64_t)C::kHalo);
-    const uint64_t f1 = warp_lower_bound(t1, flim, [&](uint64_t p) { return srec_key_toa(S, p) > toa_last + dt; });
-    if (lane == 0) {
-      const bool ftrunc = f1 == flim && flim < n && srec_key_toa(S, flim) <= toa_last + dt;
-      s_meta[1] = f1;
-      s_meta[4] = ftrunc ? srec_key_toa(S, f1) : 0;  // ToA of the first hit not staged
-      s_meta[6] = srec_key_toa(S, f1 - 1);           // largest staged ToA
-      s_meta[7] = ftrunc ? 2u : 0u;
-    }
-  } else if (threadIdx.x == 64 && t0 > 0 && (t0 % a.verify_stride) == 0) {
-    const srec p = load_srec(S + t0 - 1), q = load_srec(S + t0);
-    const uint64_t tp = srec_toa(p), tq = srec_toa(q);
-    if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&a.hdr->sort_bad, 1u);
+  // ---- staging bounds (k_tile_bounds); the tile's own records are loaded
+  // right away (they do not depend on the bounds), the halo after the barrier
+  if (threadIdx.x < 8) s_meta[threadIdx.x] = a.tile_meta[(uint64_t)blockIdx.x * 8 + threadIdx.x];
+  srec rr[C::kStage];
+#pragma unroll
+  for (int s = 0; s < C::kItems; ++s) {
+    const uint32_t l = threadIdx.x + s * kTh;
+    if (l < nt) rr[s] = load_srec(S + t0 + l);
+  }
+  if (threadIdx.x == 0) {
+    s_chunk = 0;
   }
   {
     uint4* h4 = reinterpret_cast<uint4*>(heads);
@@ -243,9 +261,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
     hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
   }
   {
-    srec rr[C::kStage];
 #pragma unroll
-    for (int s = 0; s < C::kStage; ++s) {
+    for (int s = C::kItems; s < C::kStage; ++s) {
       const uint32_t l = threadIdx.x + s * kTh;
       if (l < m) rr[s] = load_srec(S + t0 + l);
     }
@@ -280,10 +297,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
 
   // ---- neighbour search (dynamic 32-hit chunks).  Edges (j, q) with q > j
   // only: every tile pair is found from its earlier end, tile-halo pairs from
-  // the tile end; halo-halo pairs belong to the next tile.  Every edge hooks
-  // q under its smallest earlier neighbour (atomicMin: an initial forest with
-  // parent < child, ECL-CC style) and is appended to the edge list; the union
-  // pass then only needs the edges that are not hooks.
+  // the tile end; halo-halo pairs belong to the next tile.
   // flag thresholds in relative ToA (32-bit compares per hit):
   //  fwd: window continues past the staged halo  <=>  tj >= fwd_thr (if ftrunc)
   //  back: an earlier tile could reach the hit   <=>  tj <= back_thr (if t0 > 0)
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   const uint32_t back_thr = back_any ? (uint32_t)min((unsigned long long)(prev_last + dt - base), 0xffffffffull) : 0u;
   const uint32_t n_chunks = (nt + 31) / 32;
   uint16_t* eb = crank;  // per-lane edge buffers (kEdgeBuf per thread), alias of crank/aslot
-  auto search = [&](bool direct) {
+  {
     for (;;) {
       uint32_t chunk = 0;
       if (lane == 0) chunk = atomicAdd(&s_chunk, 1u);
@@ -313,17 +327,11 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         const uint2 e = rec[qq];
         const bool ok = (q > j) & (q < m) & (e.x - tj <= dt32) & adjacent(xy, e.y);
         if (ok) {
-          if (direct) {
-            s_unite(par, j, q);
+          if (ne < kEdgeBuf) {
+            eb[ne * kTh + threadIdx.x] = (uint16_t)q;
+            ++ne;
           } else {
-            atomicMin(par + q, j);
-            if (ne < kEdgeBuf) {
-              eb[ne * kTh + threadIdx.x] = (uint16_t)q;
-              ++ne;
-            } else {  // rare: straight to the CTA list
-              const uint32_t slot = atomicAdd(&s_ne, 1u);
-              if (slot < SL::kEdgeCap) elist[slot] = (j << 16) | q;
-            }
+            s_unite(par, j, q);  // rare: more than kEdgeBuf edges
           }
         }
       };
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
           visit(q);
         }
       }
-      if (!direct && act) {
+      if (act) {
         uint8_t fl = (fwd_any && tj >= fwd_thr) ? 3 : 0;  // window continues past the halo
         if (back_any && tj <= back_thr) {                 // could an earlier tile reach it?
           bool found = false;
@@ -391,35 +399,9 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         hflag[j] = fl;
       }
       __syncwarp();
-      if (direct) continue;
-      // warp-aggregated append of the lanes' buffered edges to the CTA list
-      uint32_t incl = ne;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= (unsigned)o) incl += v;
-      }
-      const uint32_t wtot = __shfl_sync(kFull, incl, 31);
-      if (wtot == 0) continue;
-      uint32_t wbase = 0;
-      if (lane == 31) wbase = atomicAdd(&s_ne, wtot);
-      wbase = __shfl_sync(kFull, wbase, 31) + incl - ne;
-      for (uint32_t k = 0; k < ne; ++k)
-        if (wbase + k < SL::kEdgeCap) elist[wbase + k] = (j << 16) | eb[k * kTh + threadIdx.x];
-    }
-  };
-  search(false);
-  __syncthreads();
-  const uint32_t ne = s_ne;
-  if (ne > SL::kEdgeCap) {  // edge list overflow (rare): unite every edge directly
-    if (threadIdx.x == 0) s_chunk = 0;
-    __syncthreads();
-    search(true);
-  } else {
-    // union pass over the non-hook edges, balanced over the CTA
-    for (uint32_t e = threadIdx.x; e < ne; e += kTh) {
-      const uint32_t v = elist[e], j = v >> 16, q = v & 0xffffu;
-      if (par[q] != j) s_unite(par, j, q);
+      // unions of the buffered edges (larger root under smaller)
+      for (uint32_t k = 0; k < ne; ++k) s_unite(par, j, eb[k * kTh + threadIdx.x]);
+      __syncwarp();
     }
   }
   __syncthreads();

@@ -39,7 +39,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 uint32_t n_tiles_of(uint64_t n, int tile) { return (uint32_t)((n + tile - 1) / tile); }
 
 struct layout {
-  size_t hdr, probe, S, parent, slot_of, stage, comp_count, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
+  size_t hdr, probe, S, parent, slot_of, stage, comp_count, tmeta, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
   size_t keys0, keys1, vals0, vals1, hist, minidx, flags, ord;
   size_t total;
   uint32_t tiles, nwords;
@@ -65,6 +65,7 @@ layout make_layout(uint64_t n) {
   L.slot_of = take(n * 4);
   L.stage = take((size_t)n_tiles_of(n, kMaxTile) * kMaxTile * 64);
   L.comp_count = take((size_t)L.tiles * 4);
+  L.tmeta = take((size_t)L.tiles * 64);
   L.open_hits = take(n * 4);
   L.open_comps = take(n * 4);
   L.overflow = take(n * 4);
@@ -297,15 +298,21 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.hdr = hdr;
   a.verify_stride = kWSortTile;
   a.phase_cycles = c->profiling >= 2 ? hdr->phase_cycles : nullptr;
+  a.tile_meta = nullptr;
   if (r.dense)
     k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
                             r.s>>>(a);
   else if (r.column)
     k_tile_cc<tile_sparse><<<n_tiles_of(r.n, tile_sparse::kTile), tile_sparse::kThreads,
                              tile_smem_bytes<tile_sparse>(), r.s>>>(a);
-  else
-    k_tile_cell<cell_sparse><<<n_tiles_of(r.n, cell_sparse::kTile), cell_sparse::kThreads,
-                               cell_smem_bytes<cell_sparse>(), r.s>>>(a);
+  else {
+    const uint32_t nt = n_tiles_of(r.n, cell_sparse::kTile);
+    a.tile_meta = (const uint64_t*)(ws + L.tmeta);
+    k_tile_bounds<cell_sparse><<<(nt + 7) / 8, 256, 0, r.s>>>(S, r.n, c->dt, nt, kWSortTile, (uint64_t*)(ws + L.tmeta),
+                                                             hdr);
+    TPX_LAUNCHED(c);
+    k_tile_cell<cell_sparse><<<nt, cell_sparse::kThreads, cell_smem_bytes<cell_sparse>(), r.s>>>(a);
+  }
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[2], r.s);
