@@ -212,4 +212,18 @@ constexpr size_t window_sort_smem() {
   return (size_t)wsort_cfg<IT>::W * 6 + (size_t)kWRadix * kWSortWarps * 4;
 }
 
+// Verification of a windowed sort right after it (before any clustering
+// work): the output is the sorted permutation iff it is strictly increasing
+// in (toa, index) at every CTA border (each CTA's range is sorted by
+// construction; n strictly increasing entries drawn from the input are a
+// permutation of it).  One thread per border.
+__global__ void k_sort_check(const srec* __restrict__ S, uint64_t n, uint32_t tile, dev_hdr* hdr) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const uint64_t b = k * tile;
+  if (b >= n) return;
+  const srec p = load_srec(S + b - 1), q = load_srec(S + b);
+  const uint64_t tp = srec_toa(p), tq = srec_toa(q);
+  if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&hdr->sort_bad, 1u);
+}
+
 }  // namespace tpx

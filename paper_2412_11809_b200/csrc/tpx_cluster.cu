@@ -98,6 +98,9 @@ struct tpx_cluster {
   cudaEvent_t ev[kMaxStages + 1];
   tpx_run_stats stats;
   int cuda_ready;  // CUDA resources are created lazily by the first run
+  int sort_start;  // first sort attempt (0: D=1024 window, 1: D=4096 window, 2: global radix);
+                   // raised to the attempt that succeeded, so a stream whose disorder exceeds
+                   // the window bound pays the failed attempts once, not on every run
   tpx_cluster* island;  // variants (b)/(c): (a)-context whose components are the islands
   uint64_t island_dt;
 };
@@ -644,16 +647,21 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   int rc;
   // attempt 0: D = 1024, attempt 1: D = 4096, attempt 2: global radix sort;
   // attempt 3: global union-find pipeline (internal fallback)
-  for (int attempt = 0; attempt < 4; ++attempt) {
+  const int first_attempt = c->sort_start;
+  for (int attempt = first_attempt; attempt < 4; ++attempt) {
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {
       k_window_sort<12><<<sort_tiles, kWSortThreads, window_sort_smem<12>(), r.s>>>(hits, n, c->width, c->height, S,
                                                                                    hdr);
       TPX_LAUNCHED(c);
+      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kWSortTile, hdr);
+      TPX_LAUNCHED(c);
     } else if (attempt == 1) {
       k_window_sort<24><<<sort_tiles, kWSortThreads, window_sort_smem<24>(), r.s>>>(hits, n, c->width, c->height, S,
                                                                                    hdr);
+      TPX_LAUNCHED(c);
+      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kWSortTile, hdr);
       TPX_LAUNCHED(c);
     } else {
       if ((rc = sort_global(c, r))) return rc;
@@ -674,7 +682,10 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       }
       if ((rc = read_header(c, r))) return rc;
       if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
-      if (attempt < 2 && c->host_hdr->sort_bad) continue;
+      if (attempt < 2 && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
+        c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
+        continue;
+      }
       if (probe_on) {
         int big = 0;
         for (int i = 0; i < kProbeSamples; ++i) big += hprobe[i] > (uint32_t)(tile_sparse::kHalo * 5 / 8);
@@ -685,7 +696,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       r.column = c->tile_mode == TPX_TILE_COLUMN;
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
-    c->stats.sort_retries = attempt < 2 ? attempt : 2;
+    c->stats.sort_retries = (attempt < 2 ? attempt : 2) - (first_attempt < 2 ? first_attempt : 2);
     // the tile kernel indexes one bucket per pixel column (sparse) or packs
     // pixel ids in 20 bits (dense): larger sensors take the global pipeline
     const bool big_sensor =
@@ -695,7 +706,10 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     if ((rc = read_header(c, r))) return rc;
     const dev_hdr& h = *c->host_hdr;
     if (h.err & 1u) return TPX_ERR_COORD_RANGE;
-    if (attempt < 2 && h.sort_bad) continue;  // displacement bound violated: widen / fall back
+    if (attempt < 2 && h.sort_bad) {  // displacement bound violated: widen / fall back
+      c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
+      continue;
+    }
     if (attempt < 3 && (h.err & 2u)) {        // tile path inconsistency: global pipeline
       attempt = 2;
       continue;
