@@ -16,20 +16,22 @@ constexpr int kListGrid = 148 * 8;
 __device__ __forceinline__ void flag_internal(dev_hdr* hdr) { atomicOr(&hdr->err, 2u); }
 
 // Hits whose forward window left the staged halo: scan the rest of the window
-// in global memory, one warp per hit (lane = candidate, 32 per step); any j it
-// reaches belongs to an open component.
+// (from the first position the tile did not stage) in global memory, one warp
+// per hit (lane = candidate, 32 per step); any j it reaches belongs to an open
+// component.
 __global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __restrict__ S, uint64_t n, uint64_t dt,
-                                                                  const uint32_t* __restrict__ list, dev_hdr* hdr,
+                                                                  const uint2* __restrict__ list, dev_hdr* hdr,
                                                                   uint32_t* parent_g) {
   const uint64_t cnt = hdr->n_overflow;
   const unsigned lane = lane_id();
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t t = wid; t < cnt; t += nw) {
-    const uint32_t i = list[t];
+    const uint2 e = list[t];
+    const uint32_t i = e.x;
     const srec a = load_srec(S + i);
     const uint64_t ta = srec_toa(a);
-    for (uint64_t j0 = (uint64_t)i + 1; j0 < n; j0 += 32) {
+    for (uint64_t j0 = e.y; j0 < n; j0 += 32) {
       const uint64_t j = j0 + lane;
       bool in = false, adj = false;
       if (j < n) {

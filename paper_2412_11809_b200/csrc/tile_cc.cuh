@@ -84,7 +84,7 @@ struct tile_args {
   uint32_t* open_hits;       // sorted positions of hits in open components
   uint32_t* open_comps;      // sorted positions of open component roots
   uint2* pairs;              // cross pairs (halo hit position, tile root position)
-  uint32_t* overflow;        // tile hits whose forward window exceeded the halo
+  uint2* overflow;           // (position, first unscanned position) of tile hits whose window exceeded the halo
   dev_hdr* hdr;
   uint32_t verify_stride;    // sorted-tile size whose borders are verified
   unsigned long long* phase_cycles;  // optional per-phase clock totals (profiling), may be null
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
                     tot * y);
         a.open_hits[oh] = (uint32_t)pos;
         a.open_comps[oc] = (uint32_t)pos;
-        a.overflow[ov] = (uint32_t)pos;
+        a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)pos + 1);
       }
     }
     if (threadIdx.x == 0) a.comp_count[blockIdx.x] = nt;
@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         a.parent_g[pos] = kSentinel;
         a.labels[rq[q].idx] = label;
       }
-      if (ovf) a.overflow[ov] = (uint32_t)pos;
+      if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
     }
   }
   TPX_PHASE(8);

@@ -127,7 +127,7 @@ __device__ __forceinline__ void tile_run_wide(const tile_args& a, uint64_t t0, u
       stage_write(a.stage + t0 + j, r.idx, own ? 1 : 0, own ? toa : ~0ull, own ? toa : 0, tot, x, y, tot * x, tot * y);
       a.open_hits[oh] = (uint32_t)pos;
       a.open_comps[oc] = (uint32_t)pos;
-      a.overflow[ov] = (uint32_t)pos;
+      a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)pos + 1);
     }
   }
   if (threadIdx.x == 0) a.comp_count[blockIdx.x] = nt;
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         a.parent_g[pos] = kSentinel;
         a.labels[tidx[q]] = label;
       }
-      if (ovf) a.overflow[ov] = (uint32_t)pos;
+      if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
     }
   }
   TPX_PHASE(8);

@@ -68,7 +68,7 @@ layout make_layout(uint64_t n) {
   L.tmeta = take((size_t)L.tiles * 64);
   L.open_hits = take(n * 4);
   L.open_comps = take(n * 4);
-  L.overflow = take(n * 4);
+  L.overflow = take(n * 8);
   L.pairs = take(n * 8);
   L.bitmap = take((size_t)L.nwords * 4);
   L.wcnt = take((size_t)L.nwords * 4);
@@ -274,7 +274,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   uint32_t* comp_count = (uint32_t*)(ws + L.comp_count);
   uint32_t* open_hits = (uint32_t*)(ws + L.open_hits);
   uint32_t* open_comps = (uint32_t*)(ws + L.open_comps);
-  uint32_t* overflow = (uint32_t*)(ws + L.overflow);
+  uint2* overflow = (uint2*)(ws + L.overflow);
   uint2* pairs = (uint2*)(ws + L.pairs);
   uint32_t* bitmap = (uint32_t*)(ws + L.bitmap);
   uint32_t* wcnt = (uint32_t*)(ws + L.wcnt);
