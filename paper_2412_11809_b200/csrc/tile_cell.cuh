@@ -103,6 +103,17 @@ __device__ __forceinline__ void add_u64_pair(uint32_t* lo, uint32_t* hi, uint64_
   if (vh) atomicAdd(hi, vh);
 }
 
+// Plain shared-memory fetch-add (the compiler would otherwise wrap a single
+// lane's atomicAdd in its warp-aggregation sequence).
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t* p, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+               : "=r"(r)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+  return r;
+}
+
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   asm volatile("" : "+r"(x));
   return x;
@@ -313,7 +324,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   {
     for (;;) {
       uint32_t chunk = 0;
-      if (lane == 0) chunk = atomicAdd(&s_chunk, 1u);
+      if (lane == 0) chunk = atom_add_shared(&s_chunk, 1u);
       chunk = __shfl_sync(kFull, chunk, 0);
       if (chunk >= n_chunks) break;
       const uint32_t j = chunk * 32 + lane;
@@ -426,8 +437,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         if (joined) copen[c] = 1;
       }
     }
-    const uint32_t slot = warp_append(joined, &a.hdr->n_pairs);
-    if (joined) a.pairs[slot] = make_uint2((uint32_t)(t0 + l), (uint32_t)(t0 + c));
+    if (__ballot_sync(kFull, joined)) {
+      const uint32_t slot = warp_append(joined, &a.hdr->n_pairs);
+      if (joined) a.pairs[slot] = make_uint2((uint32_t)(t0 + l), (uint32_t)(t0 + c));
+    }
   }
   __syncthreads();
   TPX_PHASE(4);
@@ -578,20 +591,22 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
       if (!open && label < a.n_owned) set_label_bit(a.bitmap, label);
       else a.slot_of[pos] = (uint32_t)(t0 + crank[j]);
     }
-    const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);
-    if (is_root && open) a.open_comps[oc] = (uint32_t)pos;
-    const uint32_t oh = warp_append(v && open, &a.hdr->n_open_hits);
     const bool ovf = v && (hflag[j] & 2u);
-    const uint32_t ov = warp_append(ovf, &a.hdr->n_overflow);
+    if (__ballot_sync(kFull, (v && open) || ovf)) {  // warp-uniform: most warps have no open hit
+      const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);
+      if (is_root && open) a.open_comps[oc] = (uint32_t)pos;
+      const uint32_t oh = warp_append(v && open, &a.hdr->n_open_hits);
+      const uint32_t ov = warp_append(ovf, &a.hdr->n_overflow);
+      if (v && open) a.open_hits[oh] = (uint32_t)pos;
+      if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
+    }
     if (v) {
       if (open) {
         a.parent_g[pos] = (uint32_t)(t0 + r);
-        a.open_hits[oh] = (uint32_t)pos;
       } else {
         a.parent_g[pos] = kSentinel;
         a.labels[tidx[q]] = label;
       }
-      if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
     }
   }
   TPX_PHASE(8);
