@@ -313,7 +313,7 @@ def run_ours(args):
     # paper's stream overlap); every step copies its 3.2 GB of
     # hits in and its labels + records out inside the timed region
     cap_host = max(n // 4, 1)
-    depth = 0 if args.no_e2e else 3
+    depth = 0 if args.no_e2e else args.e2e_depth
     lab_host = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(depth)]
     feat_host = [torch.empty((cap_host, 64), dtype=torch.uint8).pin_memory() for _ in range(depth)]
     del wsbuf, labels, feats
@@ -368,7 +368,7 @@ def run_ours(args):
                    "parallelism": f"{ws} GPU"},
         "e2e": {"value": round(n / (e2e_ms * 1e-3) / 1e6, 2), "unit": "Mhit/s", "h2d_bytes_per_step": n * 16,
                 "d2h_bytes_per_step": n * 4 + min(kk, cap_host) * 64, "ms_per_step": round(e2e_ms, 3),
-                "api": "tpx_pipeline_submit/wait (depth 3: copies of one buffer overlap the kernels of the others)",
+                "api": f"tpx_pipeline_submit/wait (depth {depth}: copies of one buffer overlap the kernels of the others)",
                 "steps": e2e_steps},
         "e2e_stream": stream_e2e,
         "grouped": grouped,
@@ -519,6 +519,7 @@ def main():
                     help="hits per --impl reference step (~3.5 s of single-threaded CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer legs (profiling runs only)")
+    ap.add_argument("--e2e-depth", type=int, default=3, help="tpx_pipeline slots (buffers in flight) of the e2e leg")
     ap.add_argument("--no-stream", action="store_true", help="skip the streaming host-to-host leg")
     ap.add_argument("--no-grouped", action="store_true", help="skip the grouped-output leg")
     ap.add_argument("--no-variants", action="store_true", help="skip the (iii)(b)/(c) variant legs")
