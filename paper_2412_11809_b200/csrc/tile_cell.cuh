@@ -337,14 +337,13 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         const uint32_t qq = q < m ? q : 0u;
         const uint2 e = rec[qq];
         const bool ok = (q > j) & (q < m) & (e.x - tj <= dt32) & adjacent(xy, e.y);
-        if (ok) {
-          if (ne < kEdgeBuf) {
-            eb[ne * kTh + threadIdx.x] = (uint16_t)q;
-            ++ne;
-          } else {
-            s_unite(par, j, q);  // rare: more than kEdgeBuf edges
-          }
-        }
+        // branch-free append: the slot is written every time and kept only
+        // if ok (ne advances); a full buffer unites directly (rare)
+        const uint32_t slot = ne < kEdgeBuf ? ne : kEdgeBuf - 1;
+        const bool full = ne >= kEdgeBuf;
+        if (!full) eb[slot * kTh + threadIdx.x] = (uint16_t)q;
+        ne += (ok & !full) ? 1u : 0u;
+        if (ok & full) s_unite(par, j, q);
       };
       uint64_t hq = ~0ull;  // queue of list continuations (16 bits each, kNil-padded)
       if (act) {
