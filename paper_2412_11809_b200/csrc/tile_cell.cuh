@@ -234,12 +234,22 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   // ---- staging bounds (k_tile_bounds); the tile's own records are loaded
   // right away (they do not depend on the bounds), the halo after the barrier
   if (threadIdx.x < 8) s_meta[threadIdx.x] = a.tile_meta[(uint64_t)blockIdx.x * 8 + threadIdx.x];
+  // all global loads are issued here, before the bounds are known: the tile,
+  // the largest forward halo the configuration stages (kept if < f1 after the
+  // barrier) and the largest back halo (kept if >= b0) -- one memory round
+  // trip per tile instead of three
   srec rr[C::kStage];
+  const uint64_t lim = min(n, t1 + (uint64_t)C::kHalo);
 #pragma unroll
-  for (int s = 0; s < C::kItems; ++s) {
+  for (int s = 0; s < C::kStage; ++s) {
     const uint32_t l = threadIdx.x + s * kTh;
-    if (l < nt) rr[s] = load_srec(S + t0 + l);
+    if (t0 + l < lim) rr[s] = load_srec(S + t0 + l);
   }
+  static_assert(kBackCap <= C::kThreads, "one back-halo record per thread");
+  const bool has_back = threadIdx.x < (uint32_t)kBackCap && t0 + threadIdx.x >= (uint64_t)kBackCap;
+  const uint64_t bpos = t0 + threadIdx.x - kBackCap;
+  srec rb;
+  if (has_back) rb = load_srec(S + bpos);
   if (threadIdx.x == 0) {
     s_chunk = 0;
   }
@@ -267,16 +277,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   // ---- stage: back halo; tile + forward halo into rec[] and the cell lists.
   // Tile hits' input index and ToT stay in registers (thread owns j = tid + q*kTh).
   uint32_t tidx[C::kItems], ttot[C::kItems];
-  for (uint32_t k = threadIdx.x; k < nb; k += kTh) {
-    const srec r = load_srec(S + b0 + k);
-    hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-  }
+  if (has_back && bpos >= b0) hb[bpos - b0] = make_uint2((uint32_t)(srec_toa(rb) - base), rb.xy);
   {
-#pragma unroll
-    for (int s = C::kItems; s < C::kStage; ++s) {
-      const uint32_t l = threadIdx.x + s * kTh;
-      if (l < m) rr[s] = load_srec(S + t0 + l);
-    }
 #pragma unroll
     for (int s = 0; s < C::kStage; ++s) {
       const uint32_t l = threadIdx.x + s * kTh;
