@@ -226,4 +226,146 @@ __global__ void k_sort_check(const srec* __restrict__ S, uint64_t n, uint32_t ti
   if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&hdr->sort_bad, 1u);
 }
 
+// ---------------------------------------------------------------------------
+// Windowed stable sort of (key, payload) arrays whose keys are nearly sorted
+// (every element within D positions of its place in the stable key order).
+// Used by the grouping step (group.cuh): a hit's block rank, read in the ToA
+// order S, is displaced from its output position by at most the span of its
+// cluster in S.  CTA k sorts window [kT-D, kT+T+D) by key in shared memory
+// (stable LSD radix, digits as k_window_sort) and writes the payloads of the
+// middle T; the first / last (key, position) it emits go to `edge` so a
+// border check can verify the displacement bound (k_kv_check), exactly as the
+// ToA sort is verified.
+template <int IT>
+__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort_kv(const uint32_t* __restrict__ keys,
+                                                                      const uint32_t* __restrict__ vals, uint64_t n,
+                                                                      uint32_t* __restrict__ out,
+                                                                      uint4* __restrict__ edge, dev_hdr* hdr) {
+  using C = wsort_cfg<IT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);                       // [W]
+  uint16_t* sval = reinterpret_cast<uint16_t*>(skey + C::W);                     // [W]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sval + C::W);                      // [kWRadix * warps]
+  __shared__ unsigned long long red[33];
+
+  const uint64_t k0 = (uint64_t)blockIdx.x * kWSortTile;
+  const uint64_t ws = k0 > (uint64_t)C::D ? k0 - C::D : 0;
+  const uint64_t we = min(n, k0 + kWSortTile + C::D);
+  const uint32_t m = (uint32_t)(we - ws);
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+  uint32_t key[IT];
+  uint32_t vl[IT];  // low 16 bits: window position (payload); high 16: rank within the warp
+  unsigned long long mn = ~0ull, mx = 0;
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+    key[r] = 0;
+    vl[r] = p;
+    if (p < m) {
+      key[r] = __ldg(keys + ws + p);
+      mn = min(mn, (unsigned long long)key[r]);
+      mx = max(mx, (unsigned long long)key[r]);
+    }
+  }
+  const uint32_t base = (uint32_t)block_min_u64(mn, red);
+  const uint32_t top = (uint32_t)block_max_u64(mx, red);
+  const uint32_t range = top - base;
+  const int bits = range ? 32 - __clz(range) : 0;
+  const int passes = (bits + kWDigitBits - 1) / kWDigitBits;
+#pragma unroll
+  for (int r = 0; r < IT; ++r) key[r] -= base;
+
+  __shared__ uint32_t dsum[kWSortThreads / 32];
+  for (int pass = 0; pass < passes || pass == 0; ++pass) {
+    const int shift = pass * kWDigitBits;
+    for (int i = threadIdx.x; i < kWRadix * kWSortWarps; i += kWSortThreads) cnt[i] = 0;
+    __syncthreads();
+    uint32_t* wc = cnt + warp * kWRadix;
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+      const bool valid = p < m;
+      const unsigned d = valid ? (key[r] >> shift) & (kWRadix - 1) : (unsigned)kWRadix;
+      const unsigned peers = __match_any_sync(kFull, d);
+      uint32_t b = 0;
+      if (valid) b = wc[d];
+      vl[r] = (vl[r] & 0xffffu) | ((b + __popc(peers & lanemask_lt())) << 16);
+      __syncwarp();
+      if (valid && (__ffs(peers) - 1) == (int)lane) wc[d] = b + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      uint32_t tot = 0;
+      if (threadIdx.x < kWRadix) {
+#pragma unroll
+        for (int w = 0; w < kWSortWarps; ++w) tot += cnt[w * kWRadix + threadIdx.x];
+      }
+      uint32_t x = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= (unsigned)o) x += y;
+      }
+      if (lane == 31) dsum[warp] = x;
+      __syncthreads();
+      if (threadIdx.x < kWRadix) {
+        uint32_t basev = x - tot;
+        for (unsigned w2 = 0; w2 < warp; ++w2) basev += dsum[w2];
+#pragma unroll
+        for (int w = 0; w < kWSortWarps; ++w) {
+          const uint32_t c = cnt[w * kWRadix + threadIdx.x];
+          cnt[w * kWRadix + threadIdx.x] = basev;
+          basev += c;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+      if (p < m) {
+        const unsigned d = (key[r] >> shift) & (kWRadix - 1);
+        const uint32_t q = wc[d] + (vl[r] >> 16);
+        skey[q] = key[r];
+        sval[q] = (uint16_t)vl[r];
+      }
+    }
+    __syncthreads();
+    if (pass + 1 < passes) {
+#pragma unroll
+      for (int r = 0; r < IT; ++r) {
+        const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+        if (p < m) {
+          key[r] = skey[p];
+          vl[r] = sval[p];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t ofs = (uint32_t)(k0 - ws);
+  const uint32_t cnt_out = (uint32_t)min((uint64_t)kWSortTile, n - k0);
+  for (uint32_t j = threadIdx.x; j < cnt_out; j += kWSortThreads) out[k0 + j] = __ldg(vals + ws + sval[ofs + j]);
+  if (threadIdx.x == 0) {
+    const uint32_t a = ofs, b = ofs + cnt_out - 1;
+    edge[blockIdx.x] = make_uint4(skey[a] + base, (uint32_t)(ws + sval[a]), skey[b] + base, (uint32_t)(ws + sval[b]));
+  }
+}
+
+template <int IT>
+constexpr size_t window_sort_kv_smem() {
+  return window_sort_smem<IT>();
+}
+
+// Border check of k_window_sort_kv: (key, position) strictly increasing from
+// every CTA's last output to the next CTA's first.
+__global__ void k_kv_check(const uint4* __restrict__ edge, uint32_t n_ctas, dev_hdr* hdr) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (k >= n_ctas) return;
+  const uint4 a = edge[k - 1], b = edge[k];
+  if (!(a.z < b.x || (a.z == b.x && a.w < b.y))) atomicAdd(&hdr->sort_bad, 1u);
+}
+
 }  // namespace tpx

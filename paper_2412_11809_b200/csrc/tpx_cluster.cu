@@ -130,6 +130,8 @@ static int ensure_cuda(tpx_cluster* c) {
   if (c->cuda_ready) return TPX_OK;
   if (cudaFuncSetAttribute(k_window_sort<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_smem<12>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_window_sort_kv<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)window_sort_kv_smem<12>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_window_sort<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_smem<24>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -735,6 +737,37 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
 }
 
+// G4 fallback: stable global LSD radix sort of (block index, input index)
+// on ceil(log2 k) bits.
+static int group_radix(tpx_cluster* c, uint64_t n, uint64_t k, uint32_t* k0, uint32_t* v0, uint32_t* k1,
+                       uint32_t* v1, uint32_t* hist, uint32_t* partials, uint32_t* order_out, cudaStream_t s) {
+  int rc;
+  const int bits = k > 1 ? 64 - __builtin_clzll(k - 1) : 0;
+  const int passes = bits ? (bits + 7) / 8 : 0;
+  const uint32_t tiles = n_tiles_of(n, kRadixTile);
+  if (passes == 0) {
+    TPX_CUDA(cudaMemcpyAsync(order_out, v0, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    const bool last = p == passes - 1;
+    uint32_t* vout = last ? order_out : v1;
+    k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, shift, hist, tiles);
+    TPX_LAUNCHED(c);
+    if ((rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s))) return rc;
+    k_radix_scatter<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, shift, hist, tiles, k1,
+                                                                      vout);
+    TPX_LAUNCHED(c);
+    uint32_t* t = k0;
+    k0 = k1;
+    k1 = t;
+    t = v0;
+    v0 = v1;
+    v1 = t;
+  }
+  return TPX_OK;
+}
+
 int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t* labels_out,
                             tpx_cluster_features* features_out, tpx_cluster_shape* shapes_out, uint64_t capacity,
                             uint64_t* n_clusters_out, uint32_t* order_out, uint32_t* offsets_out,
@@ -795,31 +828,30 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   k_group_rank<<<gk, 256, 0, s>>>(first, k, fbits, fbase, features_out, grank, cluster_of_out, gsize);
   TPX_LAUNCHED(c);
   if ((rc = exclusive_scan(c, gsize, k, offsets_out, partials, offsets_out + k, s))) return rc;
-  // G4: stable radix sort of (block index, input index) in S order
+  // G4: stable sort of (block index, input index) in S order.  The block
+  // index of a hit is displaced from its output place by at most its
+  // cluster's span in S, so the windowed sort does it in one pass over HBM
+  // (verified at every CTA border); the global LSD radix sort is the fallback.
   k_group_keys<<<gn, 256, 0, s>>>(S, n, cpos, grank, k0, v0);
   TPX_LAUNCHED(c);
-  const int bits = k > 1 ? 64 - __builtin_clzll(k - 1) : 0;
-  const int passes = bits ? (bits + 7) / 8 : 0;
-  const uint32_t tiles = n_tiles_of(n, kRadixTile);
-  if (passes == 0) {
-    TPX_CUDA(cudaMemcpyAsync(order_out, v0, n * 4, cudaMemcpyDeviceToDevice, s));
-  }
-  for (int p = 0; p < passes; ++p) {
-    const int shift = 8 * p;
-    const bool last = p == passes - 1;
-    uint32_t* vout = last ? order_out : v1;
-    k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, shift, hist, tiles);
+  {
+    dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
+    const uint32_t ctas = n_tiles_of(n, kWSortTile);
+    uint4* edge = (uint4*)k1;
+    TPX_CUDA(cudaMemsetAsync(&hdr->sort_bad, 0, sizeof(hdr->sort_bad), s));
+    k_window_sort_kv<12><<<ctas, kWSortThreads, window_sort_kv_smem<12>(), s>>>(k0, v0, n, order_out, edge, hdr);
     TPX_LAUNCHED(c);
-    if ((rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s))) return rc;
-    k_radix_scatter<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, shift, hist, tiles, k1,
-                                                                      vout);
-    TPX_LAUNCHED(c);
-    uint32_t* t = k0;
-    k0 = k1;
-    k1 = t;
-    t = v0;
-    v0 = v1;
-    v1 = t;
+    if (ctas > 1) {
+      k_kv_check<<<grid_for(ctas, 256), 256, 0, s>>>(edge, ctas, hdr);
+      TPX_LAUNCHED(c);
+    }
+    unsigned int bad = 0;
+    TPX_CUDA(cudaMemcpyAsync(&bad, &hdr->sort_bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    TPX_CUDA(cudaStreamSynchronize(s));
+    if (bad) {
+      c->stats.sort_retries += 1;
+      if ((rc = group_radix(c, n, k, k0, v0, k1, v1, hist, partials, order_out, s))) return rc;
+    }
   }
   // G5: shape records
   if (shapes_out) {
