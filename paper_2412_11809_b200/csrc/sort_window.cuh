@@ -236,9 +236,13 @@ __global__ void k_sort_check(const srec* __restrict__ S, uint64_t n, uint32_t ti
 // middle T; the first / last (key, position) it emits go to `edge` so a
 // border check can verify the displacement bound (k_kv_check), exactly as the
 // ToA sort is verified.
+// Keys are gathered as grank[cpos[p]] (block rank of the hit at sorted
+// position p) and payloads as S[p].idx, so the grouping needs no separate
+// key/value arrays.
 template <int IT>
-__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort_kv(const uint32_t* __restrict__ keys,
-                                                                      const uint32_t* __restrict__ vals, uint64_t n,
+__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort_kv(const uint32_t* __restrict__ cpos,
+                                                                      const uint32_t* __restrict__ grank,
+                                                                      const srec* __restrict__ S, uint64_t n,
                                                                       uint32_t* __restrict__ out,
                                                                       uint4* __restrict__ edge, dev_hdr* hdr) {
   using C = wsort_cfg<IT>;
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort_kv(const uint3
     key[r] = 0;
     vl[r] = p;
     if (p < m) {
-      key[r] = __ldg(keys + ws + p);
+      key[r] = __ldg(grank + __ldg(cpos + ws + p));
       mn = min(mn, (unsigned long long)key[r]);
       mx = max(mx, (unsigned long long)key[r]);
     }
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort_kv(const uint3
   }
   const uint32_t ofs = (uint32_t)(k0 - ws);
   const uint32_t cnt_out = (uint32_t)min((uint64_t)kWSortTile, n - k0);
-  for (uint32_t j = threadIdx.x; j < cnt_out; j += kWSortThreads) out[k0 + j] = __ldg(vals + ws + sval[ofs + j]);
+  for (uint32_t j = threadIdx.x; j < cnt_out; j += kWSortThreads) out[k0 + j] = __ldg(&S[ws + sval[ofs + j]].idx);
   if (threadIdx.x == 0) {
     const uint32_t a = ofs, b = ofs + cnt_out - 1;
     edge[blockIdx.x] = make_uint4(skey[a] + base, (uint32_t)(ws + sval[a]), skey[b] + base, (uint32_t)(ws + sval[b]));

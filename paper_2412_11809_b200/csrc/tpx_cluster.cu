@@ -98,6 +98,7 @@ struct tpx_cluster {
   cudaEvent_t ev[kMaxStages + 1];
   tpx_run_stats stats;
   int cuda_ready;  // CUDA resources are created lazily by the first run
+  int bitmap_valid;  // the last run left the label bitmap + its word scan in the workspace (tile path)
   int sort_start;  // first sort attempt (0: D=1024 window, 1: D=4096 window, 2: global radix);
                    // raised to the attempt that succeeded, so a stream whose disorder exceeds
                    // the window bound pays the failed attempts once, not on every run
@@ -703,7 +704,8 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     // pixel ids in 20 bits (dense): larger sensors take the global pipeline
     const bool big_sensor =
         c->width > (uint32_t)kBuckets || (uint64_t)c->width * c->height + c->width > kMaxTilePixels;
-    rc = (attempt == 3 || big_sensor) ? cluster_global(c, r) : cluster_sorted(c, r);
+    c->bitmap_valid = !(attempt == 3 || big_sensor);
+    rc = c->bitmap_valid ? cluster_sorted(c, r) : cluster_global(c, r);
     if (rc) return rc;
     if ((rc = read_header(c, r))) return rc;
     const dev_hdr& h = *c->host_hdr;
@@ -808,12 +810,15 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   uint32_t* partials = (uint32_t*)(ws + L.partials);
   const uint64_t nwords = L.nwords;
   const int gn = grid_for(n, 256), gk = grid_for(k, 256), gw = grid_for(nwords, 256);
-  // G0: label -> ordinal
-  k_root_bits<<<gw, 256, 0, s>>>(labels_out, n, rbits);
-  TPX_LAUNCHED(c);
-  k_popc<<<gw, 256, 0, s>>>(rbits, nwords, rbase);
-  TPX_LAUNCHED(c);
-  if ((rc = exclusive_scan(c, rbase, nwords, rbase, partials, nullptr, s))) return rc;
+  // G0: label -> ordinal (the tile path already left the label bitmap and its
+  // word scan in the workspace: bit i is set iff labels[i] == i)
+  if (!c->bitmap_valid) {
+    k_root_bits<<<gw, 256, 0, s>>>(labels_out, n, rbits);
+    TPX_LAUNCHED(c);
+    k_popc<<<gw, 256, 0, s>>>(rbits, nwords, rbase);
+    TPX_LAUNCHED(c);
+    if ((rc = exclusive_scan(c, rbase, nwords, rbase, partials, nullptr, s))) return rc;
+  }
   // G1: first sorted position per cluster
   TPX_CUDA(cudaMemsetAsync(first, 0xff, k * 4, s));
   k_group_first<<<gn, 256, 0, s>>>(S, n, labels_out, rbits, rbase, cpos, first);
@@ -832,14 +837,13 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   // index of a hit is displaced from its output place by at most its
   // cluster's span in S, so the windowed sort does it in one pass over HBM
   // (verified at every CTA border); the global LSD radix sort is the fallback.
-  k_group_keys<<<gn, 256, 0, s>>>(S, n, cpos, grank, k0, v0);
-  TPX_LAUNCHED(c);
   {
     dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
     const uint32_t ctas = n_tiles_of(n, kWSortTile);
     uint4* edge = (uint4*)k1;
     TPX_CUDA(cudaMemsetAsync(&hdr->sort_bad, 0, sizeof(hdr->sort_bad), s));
-    k_window_sort_kv<12><<<ctas, kWSortThreads, window_sort_kv_smem<12>(), s>>>(k0, v0, n, order_out, edge, hdr);
+    k_window_sort_kv<12><<<ctas, kWSortThreads, window_sort_kv_smem<12>(), s>>>(cpos, grank, S, n, order_out, edge,
+                                                                               hdr);
     TPX_LAUNCHED(c);
     if (ctas > 1) {
       k_kv_check<<<grid_for(ctas, 256), 256, 0, s>>>(edge, ctas, hdr);
@@ -850,6 +854,8 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     TPX_CUDA(cudaStreamSynchronize(s));
     if (bad) {
       c->stats.sort_retries += 1;
+      k_group_keys<<<gn, 256, 0, s>>>(S, n, cpos, grank, k0, v0);
+      TPX_LAUNCHED(c);
       if ((rc = group_radix(c, n, k, k0, v0, k1, v1, hist, partials, order_out, s))) return rc;
     }
   }
