@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
                                                               const uint32_t* __restrict__ slot_of,
                                                               const tpx_cluster_features* __restrict__ stage,
                                                               uint32_t* __restrict__ labels, uint32_t* bitmap,
-                                                              uint32_t n_owned) {
+                                                              uint32_t n_owned, uint32_t* __restrict__ first_of_label) {
   const uint64_t nh = hdr->n_open_hits, nc = hdr->n_open_comps;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh; t += stride) {
@@ -117,7 +117,11 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
     const uint32_t r = open_comps[t];
     if (parent_g[r] == r) {
       const uint32_t lab = stage[slot_of[r]].label;
-      if (lab < n_owned) set_label_bit(bitmap, lab);
+      if (lab < n_owned) {
+        set_label_bit(bitmap, lab);
+        // the final root is the smallest sorted position of the component
+        if (first_of_label) first_of_label[lab] = r;
+      }
     }
   }
 }

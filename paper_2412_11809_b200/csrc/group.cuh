@@ -58,6 +58,22 @@ __global__ void k_group_first(const srec* __restrict__ S, uint64_t n, const uint
   }
 }
 
+// G1 when the tile path recorded each cluster's first sorted position:
+// cluster ordinal per sorted position (no atomics) ...
+__global__ void k_group_cpos(const srec* __restrict__ S, uint64_t n, const uint32_t* __restrict__ labels,
+                             const uint32_t* __restrict__ rbits, const uint32_t* __restrict__ rbase,
+                             uint32_t* __restrict__ cpos) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+    cpos[p] = bit_rank(rbits, rbase, labels[__ldg(&S[p].idx)]);
+}
+
+// ... and the first position per cluster from its label.
+__global__ void k_group_first_of(const tpx_cluster_features* __restrict__ feats, uint64_t k,
+                                 const uint32_t* __restrict__ first_of_label, uint32_t* __restrict__ first) {
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < k; c += (uint64_t)gridDim.x * blockDim.x)
+    first[c] = first_of_label[feats[c].label];
+}
+
 __global__ void k_mark_first(const uint32_t* __restrict__ first, uint64_t k, uint32_t* __restrict__ fbits) {
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < k; c += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t f = first[c];

@@ -89,6 +89,7 @@ struct tile_args {
   uint32_t verify_stride;    // sorted-tile size whose borders are verified
   unsigned long long* phase_cycles;  // optional per-phase clock totals (profiling), may be null
   const uint64_t* tile_meta;  // k_tile_bounds output (k_tile_cell only)
+  uint32_t* first_of_label;   // optional (grouped runs): label -> sorted position of the cluster's first hit
 };
 
 #define TPX_PHASE(k)                                                         \
@@ -872,7 +873,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
     }
     const uint64_t pos = t0 + j;
     if (is_root) {
-      if (!open && label < a.n_owned) set_label_bit(a.bitmap, label);
+      if (!open && label < a.n_owned) {
+        set_label_bit(a.bitmap, label);
+        if (a.first_of_label) a.first_of_label[label] = (uint32_t)pos;  // grouping: cluster's first sorted position
+      }
       else a.slot_of[pos] = (uint32_t)(t0 + crank[j]);
     }
     const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);

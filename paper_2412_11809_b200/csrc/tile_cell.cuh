@@ -589,7 +589,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
     }
     const uint64_t pos = t0 + j;
     if (is_root) {
-      if (!open && label < a.n_owned) set_label_bit(a.bitmap, label);
+      if (!open && label < a.n_owned) {
+        set_label_bit(a.bitmap, label);
+        if (a.first_of_label) a.first_of_label[label] = (uint32_t)pos;  // grouping: cluster's first sorted position
+      }
       else a.slot_of[pos] = (uint32_t)(t0 + crank[j]);
     }
     const bool ovf = v && (hflag[j] & 2u);

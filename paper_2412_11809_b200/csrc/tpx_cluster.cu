@@ -99,6 +99,7 @@ struct tpx_cluster {
   tpx_run_stats stats;
   int cuda_ready;  // CUDA resources are created lazily by the first run
   int bitmap_valid;  // the last run left the label bitmap + its word scan in the workspace (tile path)
+  int want_first;    // next run records each cluster's first sorted position (grouped runs)
   int sort_start;  // first sort attempt (0: D=1024 window, 1: D=4096 window, 2: global radix);
                    // raised to the attempt that succeeded, so a stream whose disorder exceeds
                    // the window bound pays the failed attempts once, not on every run
@@ -305,6 +306,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.verify_stride = kWSortTile;
   a.phase_cycles = c->profiling >= 2 ? hdr->phase_cycles : nullptr;
   a.tile_meta = nullptr;
+  a.first_of_label = c->want_first ? (uint32_t*)(ws + L.minidx) : nullptr;
   if (r.dense)
     k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
                             r.s>>>(a);
@@ -331,7 +333,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   k_merge_open<<<kListGrid, kListThreads, 0, r.s>>>(open_comps, hdr, parent_g, slot_of, stage);
   TPX_LAUNCHED(c);
   k_open_labels<<<kListGrid, kListThreads, 0, r.s>>>(S, open_hits, open_comps, hdr, parent_g, slot_of, stage,
-                                                     r.labels, bitmap, (uint32_t)r.n_owned);
+                                                     r.labels, bitmap, (uint32_t)r.n_owned, a.first_of_label);
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[3], r.s);
@@ -781,8 +783,10 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       ((uintptr_t)shapes_out & 15))
     return TPX_ERR_INVALID_ARG;
   uint64_t k = 0;
+  c->want_first = 1;
   int rc = tpx_cluster_run_partial(c, hits, n, n, labels_out, features_out, capacity, &k, workspace,
                                    workspace_bytes, stream);
+  c->want_first = 0;
   *n_clusters_out = k;
   cudaStream_t s = (cudaStream_t)stream;
   if (rc == TPX_OK && n == 0 && offsets_out) {
@@ -798,7 +802,8 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   uint32_t* rbase = (uint32_t*)(ws + L.wcnt);
   uint32_t* fbits = (uint32_t*)(ws + L.open_hits);
   uint32_t* fbase = (uint32_t*)(ws + L.open_comps);
-  uint32_t* cpos = (uint32_t*)(ws + L.minidx);
+  uint32_t* cpos = (uint32_t*)(ws + L.keys1);        // per sorted position (k1 is free until the fallback)
+  const uint32_t* first_of_label = (const uint32_t*)(ws + L.minidx);  // written by the run (tile path)
   uint32_t* first = (uint32_t*)(ws + L.flags);
   uint32_t* grank = (uint32_t*)(ws + L.ord);
   uint32_t* gsize = (uint32_t*)(ws + L.parent);
@@ -819,10 +824,18 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     TPX_LAUNCHED(c);
     if ((rc = exclusive_scan(c, rbase, nwords, rbase, partials, nullptr, s))) return rc;
   }
-  // G1: first sorted position per cluster
-  TPX_CUDA(cudaMemsetAsync(first, 0xff, k * 4, s));
-  k_group_first<<<gn, 256, 0, s>>>(S, n, labels_out, rbits, rbase, cpos, first);
-  TPX_LAUNCHED(c);
+  // G1: first sorted position per cluster (recorded by the tile path; atomics
+  // over all hits otherwise)
+  if (c->bitmap_valid) {
+    k_group_cpos<<<gn, 256, 0, s>>>(S, n, labels_out, rbits, rbase, cpos);
+    TPX_LAUNCHED(c);
+    k_group_first_of<<<gk, 256, 0, s>>>(features_out, k, first_of_label, first);
+    TPX_LAUNCHED(c);
+  } else {
+    TPX_CUDA(cudaMemsetAsync(first, 0xff, k * 4, s));
+    k_group_first<<<gn, 256, 0, s>>>(S, n, labels_out, rbits, rbase, cpos, first);
+    TPX_LAUNCHED(c);
+  }
   // G2/G3: block index of each cluster, block table, offsets
   TPX_CUDA(cudaMemsetAsync(fbits, 0, nwords * 4, s));
   k_mark_first<<<gk, 256, 0, s>>>(first, k, fbits);
@@ -840,7 +853,7 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   {
     dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
     const uint32_t ctas = n_tiles_of(n, kWSortTile);
-    uint4* edge = (uint4*)k1;
+    uint4* edge = (uint4*)hist;
     TPX_CUDA(cudaMemsetAsync(&hdr->sort_bad, 0, sizeof(hdr->sort_bad), s));
     k_window_sort_kv<12><<<ctas, kWSortThreads, window_sort_kv_smem<12>(), s>>>(cpos, grank, S, n, order_out, edge,
                                                                                hdr);
