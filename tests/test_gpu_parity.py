@@ -197,10 +197,43 @@ def test_empty_and_degenerate(tpx):
     _assert_parity(tpx, h, 320, ctx="wide toa")
 
 
+def _fresh(tpx, h, dt, W=256, H=256):
+    c = tpx.Clusterer(dt, W, H)
+    d = torch.from_numpy(np.ascontiguousarray(h).view(np.uint8).reshape(-1)).cuda()
+    labels, feats, k = c.run(d, n=len(h))
+    torch.cuda.synchronize()
+    return c, labels.cpu().numpy().view(np.uint32)[:len(h)], tpx.features_to_numpy(feats), k
+
+
 def test_disorder_stress(tpx):
-    # paper-bound readout disorder t = 600 us
+    # paper-bound readout disorder t = 600 us; a fresh
+    # context, so the shared ones keep starting with the windowed sort
     h = tpxgen.generate("mixed", n_hits=2_000_000, disorder_ticks=384_000)
-    _assert_parity(tpx, h, 320, ctx="J=600us")
+    c, gl, gf, k = _fresh(tpx, h, 320)
+    rl, rf = oracle.cluster(h, 320)
+    assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
+
+
+def test_sort_attempt_memory(tpx):
+    """A failed displacement bound is detected right after the sort (no
+    clustering pass on a wrong order) and the context starts at the attempt
+    that succeeded on later runs; results stay exact on any later stream."""
+    h_bad = tpxgen.generate("mixed", n_hits=1_500_000, disorder_ticks=384_000)
+    c, gl, gf, k = _fresh(tpx, h_bad, 320)
+    st1 = c.stats()
+    assert st1["sort_retries"] >= 1
+    d = torch.from_numpy(h_bad.view(np.uint8)).cuda()
+    c.run(d)
+    st2 = c.stats()
+    assert st2["sort_retries"] == 0 and st2["sort_path"] == st1["sort_path"]
+    # the same context on a well-ordered stream: still exact
+    h_ok = tpxgen.generate("mixed", n_hits=1_000_000)
+    d = torch.from_numpy(h_ok.view(np.uint8)).cuda()
+    labels, feats, k = c.run(d)
+    torch.cuda.synchronize()
+    rl, rf = oracle.cluster(h_ok, 320)
+    assert np.array_equal(labels.cpu().numpy().view(np.uint32), rl)
+    assert tpx.features_to_numpy(feats).tobytes() == rf.tobytes()
 
 
 def test_coord_range_error(tpx):
