@@ -336,10 +336,13 @@ def run_ours(args):
     dom = max(stage_avg, key=stage_avg.get) if stage_avg else None
     peak, peak_src = _peaks()
     traffic = None
+    warp_inst = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if dom and os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(dom)
+            tj = json.load(open(tfile))
+            traffic = tj.get(dom)
+            warp_inst = tj.get(dom + "_warp_inst")
         except Exception:
             traffic = None
     roof = None
@@ -348,6 +351,17 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_hit": round(b_alg_hit, 3), "launch_ms": round(stage_avg[dom], 4)}
+        # the bound that actually limits this kernel: instruction issue (it is
+        # integer / shared-memory / control work, not bytes): ncu's warp
+        # instructions per launch over the live-timed launch, against 4
+        # schedulers x 148 SMs x the SM clock sampled during the timed region
+        if warp_inst:
+            sm_hz = ((clocks or {}).get("sm_mhz") or 1965.0) * 1e6
+            issue_peak = 4 * 148 * sm_hz
+            issue = warp_inst / (stage_avg[dom] * 1e-3)
+            roof["issue"] = {"achieved_warp_inst_per_s": round(issue / 1e9, 1), "peak_warp_inst_per_s": round(issue_peak / 1e9, 1),
+                             "unit": "G warp-inst/s", "frac": round(issue / issue_peak, 4),
+                             "warp_inst_per_launch": warp_inst, "source": "profiles/traffic.json (ncu smsp__inst_executed.sum)"}
     whole_path_gbs = b_alg_hit * n / (ms * 1e-3) / 1e9
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
