@@ -37,33 +37,45 @@ class ShardError(RuntimeError):
 
 # ---------------------------------------------------------------- communicators
 class TorchComm:
-    """torch.distributed process group (NCCL on GPUs, gloo on CPU)."""
+    """torch.distributed process group (NCCL on GPUs, gloo on CPU).
 
-    def __init__(self, group=None):
+    ``staged=True`` routes device tensors through host memory for every
+    collective -- a gloo process group on GPU ranks (functional runs of the
+    multi-process path where NCCL is unavailable, e.g. several ranks sharing
+    one GPU); the NVLink path is NCCL with staged=False."""
+
+    def __init__(self, group=None, staged: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
+        self.staged = staged
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
     def allgather(self, t):
         """All-gather equal-shape tensors -> list (rank order)."""
-        out = [t.new_empty(t.shape) for _ in range(self.world)]
-        self.dist.all_gather(out, t.contiguous(), group=self.group)
-        return out
+        src = t.contiguous().cpu() if self.staged else t.contiguous()
+        out = [src.new_empty(src.shape) for _ in range(self.world)]
+        self.dist.all_gather(out, src, group=self.group)
+        return [o.to(t.device) for o in out] if self.staged else out
 
     def exchange(self, send_to, send_tensors, recv_from, recv_tensors):
         """Point-to-point: send a list to one peer, receive a list from another."""
         ops = []
         P2POp, isend, irecv = self.dist.P2POp, self.dist.isend, self.dist.irecv
+        sends = [t.contiguous().cpu() if self.staged else t.contiguous() for t in send_tensors]
+        recvs = [t.new_empty(t.shape, device="cpu") if self.staged else t for t in recv_tensors]
         if send_to is not None:
-            ops += [P2POp(isend, t.contiguous(), send_to, self.group) for t in send_tensors]
+            ops += [P2POp(isend, t, send_to, self.group) for t in sends]
         if recv_from is not None:
-            ops += [P2POp(irecv, t, recv_from, self.group) for t in recv_tensors]
+            ops += [P2POp(irecv, t, recv_from, self.group) for t in recvs]
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
+        if self.staged and recv_from is not None:
+            for dst, src in zip(recv_tensors, recvs):
+                dst.copy_(src)
 
     def barrier(self):
         self.dist.barrier(group=self.group)
