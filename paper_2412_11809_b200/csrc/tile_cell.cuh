@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   const uint64_t t0 = (uint64_t)blockIdx.x * kT;
   const uint64_t t1 = min(n, t0 + kT);
   const uint32_t nt = (uint32_t)(t1 - t0);
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lane = lane_id();
   long long t_phase = clock64();
 
   // ---- staging bounds (k_tile_bounds); the tile's own records are loaded
@@ -270,7 +270,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   }
   const uint32_t nb = (uint32_t)(t0 - b0);
   const uint32_t m = (uint32_t)(f1 - t0);  // tile + forward halo
-  const uint32_t nf = m - nt;
   const uint32_t dt32 = dt > 0xffffffffull ? 0xffffffffu : (uint32_t)dt;
   const uint32_t wmax = a.width - 1, hmax = a.height - 1;
 
