@@ -100,7 +100,7 @@ struct tpx_cluster {
   int cuda_ready;  // CUDA resources are created lazily by the first run
   int bitmap_valid;  // the last run left the label bitmap + its word scan in the workspace (tile path)
   int want_first;    // next run records each cluster's first sorted position (grouped runs)
-  int sort_start;  // first sort attempt (0: D=1024 window, 1: D=4096 window, 2: global radix);
+  int sort_start;  // first sort attempt (0: D=1024 window, 1: D=3072 window, 2: global radix);
                    // raised to the attempt that succeeded, so a stream whose disorder exceeds
                    // the window bound pays the failed attempts once, not on every run
   tpx_cluster* island;  // variants (b)/(c): (a)-context whose components are the islands
@@ -134,8 +134,8 @@ static int ensure_cuda(tpx_cluster* c) {
                            (int)window_sort_smem<12>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_window_sort_kv<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_kv_smem<12>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_window_sort<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)window_sort_smem<24>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_window_sort<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)window_sort_smem<20>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_dense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -650,7 +650,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   const uint32_t sort_tiles = n_tiles_of(n, kWSortTile);
 
   int rc;
-  // attempt 0: D = 1024, attempt 1: D = 4096, attempt 2: global radix sort;
+  // attempt 0: D = 1024, attempt 1: D = 3072, attempt 2: global radix sort;
   // attempt 3: global union-find pipeline (internal fallback)
   const int first_attempt = c->sort_start;
   for (int attempt = first_attempt; attempt < 4; ++attempt) {
@@ -663,7 +663,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kWSortTile, hdr);
       TPX_LAUNCHED(c);
     } else if (attempt == 1) {
-      k_window_sort<24><<<sort_tiles, kWSortThreads, window_sort_smem<24>(), r.s>>>(hits, n, c->width, c->height, S,
+      k_window_sort<20><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width, c->height, S,
                                                                                    hdr);
       TPX_LAUNCHED(c);
       k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kWSortTile, hdr);
