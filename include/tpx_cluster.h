@@ -127,8 +127,14 @@ int tpx_cluster_workspace_bytes(const tpx_cluster* ctx, uint64_t n,
  *   workspace    DEVICE, >= tpx_cluster_workspace_bytes(n), 256-B aligned.
  *   stream       cudaStream_t (NULL = legacy default stream).
  * All work is stream-ordered on `stream`; the call returns after the cluster
- * count has been read back (one small device->host copy + stream sync).
- * n = 0 returns TPX_OK with 0 clusters.  The caller owns every buffer. */
+ * count has been read back (one small device->host copy + stream sync; a
+ * second one after the sort carries its verification and the window-density
+ * probe).  The windowed sort is verified before any clustering work; when its
+ * displacement bound fails the run retries with a wider window, then the global
+ * radix sort, and the context starts later runs at the attempt that succeeded
+ * (results are identical on every path; tpx_run_stats reports the path).
+ * n = 0 returns TPX_OK with 0 clusters.  The caller owns every buffer.
+ * Not thread-safe per context (one context per stream). */
 int tpx_cluster_run(tpx_cluster* ctx, const tpx_hit* hits, uint64_t n,
                     uint32_t* labels_out, tpx_cluster_features* features_out,
                     uint64_t capacity, uint64_t* n_clusters_out,
@@ -216,7 +222,9 @@ typedef struct tpx_run_stats {
   uint64_t n_clusters;
   uint32_t sort_path;      /* 0 = windowed bounded-disorder sort,
                               1 = global radix fallback                      */
-  uint32_t sort_retries;   /* windowed attempts that failed verification     */
+  uint32_t sort_retries;   /* windowed attempts that failed verification in
+                              this run (grouped runs: + 1 if the windowed
+                              key sort of the grouping fell back)            */
   uint64_t cross_pairs;    /* tile-border union pairs processed              */
   uint32_t kernel_launches;/* kernels launched by the last run               */
   uint32_t n_stages;       /* valid entries in stage_ms / stage names        */
