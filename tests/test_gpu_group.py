@@ -40,6 +40,7 @@ def _check(tpx, h, dt, W=256, H=256, ctx=""):
     bad = np.nonzero(go != ro)[0]
     assert len(bad) == 0, f"{ctx}: order differs at {bad[:5]}"
     assert tpx.shapes_to_numpy(sh).tobytes() == rs.tobytes(), ctx
+    return c.stats()
 
 
 def test_group_small_fuzz(tpx):
@@ -66,3 +67,25 @@ def test_group_edge_cases(tpx):
     _check(tpx, tpxgen.generate("mixed", n_hits=70_000), 100_000, ctx="giant clusters")
     # > 2^16 clusters (three radix passes of the block index)
     _check(tpx, tpxgen.generate("lowflux", n_hits=2_000_000), 128, ctx="many clusters")
+
+
+def test_group_key_sort_paths(tpx):
+    """Both ways of ordering the blocks: the windowed key sort (clusters span
+    few sorted positions) and its radix fallback (a cluster spanning more
+    than the 1024-position window bound), each exact."""
+    st = _check(tpx, tpxgen.generate("mixed", n_hits=400_000), 320, ctx="windowed key sort")
+    assert st["sort_retries"] == 0
+    # one chain cluster on a single pixel row, interleaved with a background
+    # of isolated hits: its hits span > 1024 sorted positions
+    rng = np.random.default_rng(11)
+    n_bg, n_chain = 60_000, 3_000
+    bg = np.zeros(n_bg, dtype=tpxgen.HIT_DTYPE)
+    bg["x"], bg["y"] = rng.integers(0, 256, n_bg), rng.integers(0, 100, n_bg)
+    bg["toa"], bg["tot"] = np.sort(rng.integers(0, 60 * n_chain, n_bg)), 5
+    ch = np.zeros(n_chain, dtype=tpxgen.HIT_DTYPE)
+    ch["x"], ch["y"], ch["toa"], ch["tot"] = np.arange(n_chain) % 256, 200 + (np.arange(n_chain) // 256) % 50, \
+        np.arange(n_chain) * 60, 7
+    h = np.concatenate([bg, ch])
+    h = h[np.argsort(h["toa"], kind="stable")]
+    st = _check(tpx, h, 60, ctx="long chain")
+    assert st["sort_retries"] >= 1
