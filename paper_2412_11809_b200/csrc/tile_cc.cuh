@@ -33,10 +33,12 @@
 namespace tpx {
 
 constexpr int kTile = 1024;                    // smallest tile (comp_count sizing)
-constexpr int kMaxTile = 2048;                 // largest tile (stage slot sizing)
+constexpr int kMaxTile = 4096;                 // largest tile (stage slot sizing)
 constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
-constexpr uint32_t kPixEmpty = 0xfffffu;       // empty hash slot key (pixel ids must be < 2^20 - 1)
-constexpr uint32_t kMaxTilePixels = 0xfffffu;  // sensors with more pixels take the global path
+constexpr int kHeadBits = 13;                  // dense pixel hash: slot word = pixel << 13 | list head
+constexpr uint32_t kHeadMask = (1u << kHeadBits) - 1;
+constexpr uint32_t kPixEmpty = 0xffffffffu >> kHeadBits;  // empty hash slot key (pixel ids must be < 2^19 - 1)
+constexpr uint32_t kMaxTilePixels = kPixEmpty - 1;  // sensors with more pixels take the global path
 constexpr uint16_t kNil = 0xffffu;             // end of a pixel list
 constexpr int kBuckets = 1024;                 // sparse: one bucket per pixel column (wider sensors: global path)
 constexpr int kBucketCap = 512;                // sparse: longer buckets take the global path
@@ -58,15 +60,15 @@ struct tile_cfg {
   static constexpr bool kRegStage = kStageItems <= 8;             // stage in registers, else re-read S
   static constexpr int kBlocks = kMinBlocks;
   static constexpr bool kHash = kHashIndex;                       // pixel hash (dense) vs column buckets (sparse)
-  static constexpr int kSlotBits = kFwdMax <= 2048 ? 12 : 13;     // pixel hash slots (load <= 1/2)
+  static constexpr int kSlotBits = kFwdMax <= 2048 ? 12 : kFwdMax <= 4096 ? 13 : 14;  // pixel hash slots (load <= 1/2)
   static constexpr int kSlots = 1 << kSlotBits;
   static_assert(kFwdMax % kThreads == 0 && kTile % kThreads == 0 && kTile % ::tpx::kTile == 0 &&
                     kTile <= kMaxTile, "staging layout");
-  static_assert(kFwdMax <= 4096, "12-bit list heads");
+  static_assert(kFwdMax <= (1 << kHeadBits), "13-bit list heads");
   static_assert(kSlots >= 2 * kFwdMax, "hash load");
 };
 using tile_sparse = tile_cfg<1024, 256, 1024, 4, false>;
-using tile_dense = tile_cfg<2048, 512, 2048, 2, true>;
+using tile_dense = tile_cfg<4096, 1024, 4096, 1, true>;
 
 struct tile_args {
   const srec* S;
@@ -225,7 +227,7 @@ struct tile_smem_hash {
   static constexpr size_t kFwdMax = C::kFwdMax;
   static constexpr size_t kTile = C::kTile;
   static constexpr size_t kTileThreads = C::kThreads;
-  static constexpr size_t tab = 0;                                      // u32 [kSlots] pixel << 12 | list head
+  static constexpr size_t tab = 0;                                      // u32 [kSlots] pixel << 13 | list head
   static constexpr size_t stoa = tab + (size_t)C::kSlots * 4;           // u32 [kFwdMax] toa - base
   static constexpr size_t nxt = stoa + (size_t)kFwdMax * 4;             // u16 [kFwdMax] next in pixel list
   static constexpr size_t sxy = nxt + (size_t)kFwdMax * 2;              // u32 [kTile]   y << 16 | x
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   uint16_t* myrank = nullptr; // local index -> csort position
   uint32_t* bs = nullptr;     // bucket counts, then bucket starts
   uint32_t* cltmp = nullptr;  // unranked bucket entries (alias of par)
-  uint32_t* tab = nullptr;    // pixel hash: pixel << 12 | list head, open addressing
+  uint32_t* tab = nullptr;    // pixel hash: pixel << 13 | list head, open addressing
   uint32_t* stoa = nullptr;   // toa - base by local index
   uint16_t* nxt = nullptr;    // next local index on the same pixel
   uint32_t* sxy = nullptr;    // y << 16 | x of tile hits
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   }
   if constexpr (C::kHash) {
     // ---- stage: back halo; tile + forward halo into a pixel hash index.  Each
-    // occupied pixel owns one open-addressing slot (pixel << 12 | head) and a
+    // occupied pixel owns one open-addressing slot (pixel << 13 | head) and a
     // list of its local indices threaded through nxt[] -- a compact, per-CTA
     // stand-in for the paper's 256x256 "last hit per pixel" matrix (P:171,
     // P:310).  Inserts are lock-free pushes (atomicCAS on the slot word).
@@ -588,14 +590,14 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       uint32_t h = slot_of_pixel(pix);
       uint32_t cur = tab[h];
       for (;;) {
-        const uint32_t ck = cur >> 12;
+        const uint32_t ck = cur >> kHeadBits;
         if (ck != kPixEmpty && ck != pix) {  // another pixel: linear probing
           h = (h + 1) & (C::kSlots - 1);
           cur = tab[h];
           continue;
         }
-        nxt[l] = ck == pix ? (uint16_t)(cur & 0xfffu) : kNil;
-        const uint32_t old = atomicCAS(tab + h, cur, (pix << 12) | l);
+        nxt[l] = ck == pix ? (uint16_t)(cur & kHeadMask) : kNil;
+        const uint32_t old = atomicCAS(tab + h, cur, (pix << kHeadBits) | l);
         if (old == cur) break;
         cur = old;
       }
@@ -672,13 +674,13 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
             const uint32_t pix = (y + dy) * W + (x + dx);
             uint32_t h = slot_of_pixel(pix);
             uint32_t cur;
-            while (((cur = tab[h]) >> 12) != pix) {
-              if ((cur >> 12) == kPixEmpty) break;
+            while (((cur = tab[h]) >> kHeadBits) != pix) {
+              if ((cur >> kHeadBits) == kPixEmpty) break;
               h = (h + 1) & (C::kSlots - 1);
             }
-            if ((cur >> 12) != pix) continue;
+            if ((cur >> kHeadBits) != pix) continue;
             uint32_t best = 0xffffu;
-            for (uint32_t q = cur & 0xfffu; q != kNil; q = nxt[q])
+            for (uint32_t q = cur & kHeadMask; q != kNil; q = nxt[q])
               if (q > j && q < best) best = q;
             if (best != 0xffffu && stoa[best] - tj <= dt32) edge(best);
           }
