@@ -35,9 +35,9 @@ namespace tpx {
 constexpr int kTile = 1024;                    // smallest tile (comp_count sizing)
 constexpr int kMaxTile = 4096;                 // largest tile (stage slot sizing)
 constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
-constexpr int kHeadBits = 13;                  // dense pixel hash: slot word = pixel << 13 | list head
+constexpr int kHeadBits = 14;                  // dense pixel hash: slot word = pixel << 14 | list head
 constexpr uint32_t kHeadMask = (1u << kHeadBits) - 1;
-constexpr uint32_t kPixEmpty = 0xffffffffu >> kHeadBits;  // empty hash slot key (pixel ids must be < 2^19 - 1)
+constexpr uint32_t kPixEmpty = 0xffffffffu >> kHeadBits;  // empty hash slot key (pixel ids must be < 2^18 - 1)
 constexpr uint32_t kMaxTilePixels = kPixEmpty - 1;  // sensors with more pixels take the global path
 constexpr uint16_t kNil = 0xffffu;             // end of a pixel list
 constexpr int kBuckets = 1024;                 // sparse: one bucket per pixel column (wider sensors: global path)
@@ -64,7 +64,7 @@ struct tile_cfg {
   static constexpr int kSlots = 1 << kSlotBits;
   static_assert(kFwdMax % kThreads == 0 && kTile % kThreads == 0 && kTile % ::tpx::kTile == 0 &&
                     kTile <= kMaxTile, "staging layout");
-  static_assert(kFwdMax <= (1 << kHeadBits), "13-bit list heads");
+  static_assert(kFwdMax + 256 <= (1 << kHeadBits), "list heads: tile + halos fit kHeadBits");
   static_assert(kSlots >= 2 * kFwdMax, "hash load");
 };
 using tile_sparse = tile_cfg<1024, 256, 1024, 4, false>;
@@ -227,10 +227,11 @@ struct tile_smem_hash {
   static constexpr size_t kFwdMax = C::kFwdMax;
   static constexpr size_t kTile = C::kTile;
   static constexpr size_t kTileThreads = C::kThreads;
-  static constexpr size_t tab = 0;                                      // u32 [kSlots] pixel << 13 | list head
-  static constexpr size_t stoa = tab + (size_t)C::kSlots * 4;           // u32 [kFwdMax] toa - base
-  static constexpr size_t nxt = stoa + (size_t)kFwdMax * 4;             // u16 [kFwdMax] next in pixel list
-  static constexpr size_t sxy = nxt + (size_t)kFwdMax * 2;              // u32 [kTile]   y << 16 | x
+  static constexpr size_t tab = 0;                                      // u32 [kSlots] pixel << 14 | list head
+  static constexpr size_t kIdx = kFwdMax + kBackCap;                    // local indices: tile + fwd halo, then back halo
+  static constexpr size_t stoa = tab + (size_t)C::kSlots * 4;           // u32 [kIdx] toa - base
+  static constexpr size_t nxt = stoa + kIdx * 4;                        // u16 [kIdx] next in pixel list
+  static constexpr size_t sxy = nxt + kIdx * 2;                         // u32 [kTile]   y << 16 | x
   static constexpr size_t region_a = sxy + (size_t)kTile * 4;
   // reduction-phase aliases of region A
   static constexpr size_t stile = 0;                                    // uint4 [kTile]
@@ -602,10 +603,31 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         cur = old;
       }
     };
+    // back-halo hits go into the same pixel lists with local indices m + k:
+    // a tile hit finds the earlier hits next to it through its 9 lookups
+    // instead of scanning the back halo
+    auto insert_back = [&](uint32_t l, uint2 e) {
+      stoa[l] = e.x;
+      const uint32_t pix = (e.y >> 16) * W + (e.y & 0xffffu);
+      uint32_t h = slot_of_pixel(pix);
+      uint32_t cur = tab[h];
+      for (;;) {
+        const uint32_t ck = cur >> kHeadBits;
+        if (ck != kPixEmpty && ck != pix) {
+          h = (h + 1) & (C::kSlots - 1);
+          cur = tab[h];
+          continue;
+        }
+        nxt[l] = ck == pix ? (uint16_t)(cur & kHeadMask) : kNil;
+        const uint32_t old = atomicCAS(tab + h, cur, (pix << kHeadBits) | l);
+        if (old == cur) break;
+        cur = old;
+      }
+    };
     if (!wide) {
       for (uint32_t k = threadIdx.x; k < nb; k += kTileThreads) {
         const srec r = load_srec(S + b0 + k);
-        hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
+        insert_back(m + k, make_uint2((uint32_t)(srec_toa(r) - base), r.xy));
       }
       if constexpr (C::kRegStage) {
         uint2 ev[kStageItems];
@@ -661,6 +683,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
         else s_unite(par, j, lj);
       };
+      bool back_near = false;
       if constexpr (C::kHash) {
         xy = sxy[j];
         tj = stoa[j];
@@ -680,8 +703,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
             }
             if ((cur >> kHeadBits) != pix) continue;
             uint32_t best = 0xffffu;
-            for (uint32_t q = cur & kHeadMask; q != kNil; q = nxt[q])
-              if (q > j && q < best) best = q;
+            for (uint32_t q = cur & kHeadMask; q != kNil; q = nxt[q]) {
+              if (q >= m) back_near |= tj - stoa[q] <= dt32;  // back-halo hit (earlier)
+              else if (q > j && q < best) best = q;
+            }
             if (best != 0xffffu && stoa[best] - tj <= dt32) edge(best);
           }
         }
@@ -712,7 +737,11 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       }
       uint8_t fl = 0;
       if (ftrunc && first_unstaged <= base + tj + dt) fl = 3;  // window continues past the halo
-      if (t0 > 0 && base + tj <= prev_last + dt) {           // could an earlier tile reach it?
+      if constexpr (C::kHash) {
+        // adjacent back-halo hit within dt, or a truncated back halo whose
+        // earliest staged hit (relative ToA 0) is still within dt
+        if (back_near || (t0 > 0 && btrunc && tj <= dt32)) fl |= 1;
+      } else if (t0 > 0 && base + tj <= prev_last + dt) {  // could an earlier tile reach it?
         bool found = false;
         int lb = (int)nb - 1;
         for (; lb >= 0; --lb) {
