@@ -25,10 +25,17 @@ constexpr int kWDigitBits = 9;     // radix digit: 512 bins, so a 18-bit window 
 constexpr int kWRadix = 1 << kWDigitBits;
 static_assert(kWRadix <= kWSortThreads, "one scan thread per digit");
 
-template <int IT>
+// windowed sort attempts of tpx_cluster_run: 0 -> 8192 outputs per CTA from
+// a 10240-hit window (IT = 20, D = 1024, 1.25x redundancy); 1 -> 4096 outputs
+// from the same window (D = 3072, Timepix4-rate streams)
+constexpr int kSortT0 = 8192;
+constexpr int kSortT1 = 4096;
+
+template <int IT, int T = kWSortTile>
 struct wsort_cfg {
   static constexpr int W = kWSortThreads * IT;         // window capacity
-  static constexpr int D = (W - kWSortTile) / 2;       // displacement bound
+  static constexpr int kT = T;                         // output records per CTA
+  static constexpr int D = (W - T) / 2;                // displacement bound
   static constexpr int PER_WARP = IT * 32;
 };
 
@@ -66,20 +73,20 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
   return r;
 }
 
-template <int IT>
+template <int IT, int T>
 __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit* __restrict__ hits, uint64_t n,
                                                                    uint32_t width, uint32_t height,
                                                                    srec* __restrict__ out, dev_hdr* hdr) {
-  using C = wsort_cfg<IT>;
+  using C = wsort_cfg<IT, T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);                       // [W]
   uint16_t* sval = reinterpret_cast<uint16_t*>(skey + C::W);                     // [W]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sval + C::W);                      // [kWRadix * warps]
   __shared__ unsigned long long red[33];
 
-  const uint64_t k0 = (uint64_t)blockIdx.x * kWSortTile;
+  const uint64_t k0 = (uint64_t)blockIdx.x * T;
   const uint64_t ws = k0 > (uint64_t)C::D ? k0 - C::D : 0;
-  const uint64_t we = min(n, k0 + kWSortTile + C::D);
+  const uint64_t we = min(n, k0 + T + C::D);
   const uint32_t m = (uint32_t)(we - ws);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
 
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
 
   // ---- write the middle T records (window-local ranks [k0-ws, k0-ws+T))
   const uint32_t ofs = (uint32_t)(k0 - ws);
-  const uint32_t cnt_out = (uint32_t)min((uint64_t)kWSortTile, n - k0);
+  const uint32_t cnt_out = (uint32_t)min((uint64_t)T, n - k0);
   for (uint32_t j = threadIdx.x; j < cnt_out; j += kWSortThreads) {
     const uint64_t gi = ws + sval[ofs + j];
     hit4 h = load_hit(hits + gi);

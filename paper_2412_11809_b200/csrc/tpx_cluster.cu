@@ -130,11 +130,11 @@ struct tpx_cluster {
 // that contexts can be created (and arguments validated) without a GPU.
 static int ensure_cuda(tpx_cluster* c) {
   if (c->cuda_ready) return TPX_OK;
-  if (cudaFuncSetAttribute(k_window_sort<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)window_sort_smem<12>()) != cudaSuccess ||
+  if (cudaFuncSetAttribute(k_window_sort<20, kSortT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)window_sort_smem<20>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_window_sort_kv<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_kv_smem<12>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_window_sort<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_window_sort<20, kSortT1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_smem<20>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
@@ -224,6 +224,7 @@ struct run_ptrs {
   layout L;
   cudaStream_t s;
   bool dense;   // tile configuration chosen by the density probe
+  uint32_t sort_T = kWSortTile;  // output tile of the sort that produced S (its borders are verified)
   bool column;  // legacy column-bucket sparse kernel (TPX_TILE_COLUMN, comparison only)
 };
 
@@ -303,7 +304,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.pairs = pairs;
   a.overflow = overflow;
   a.hdr = hdr;
-  a.verify_stride = kWSortTile;
+  a.verify_stride = r.sort_T;
   a.phase_cycles = c->profiling >= 2 ? hdr->phase_cycles : nullptr;
   a.tile_meta = nullptr;
   a.first_of_label = c->want_first ? (uint32_t*)(ws + L.minidx) : nullptr;
@@ -316,7 +317,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   else {
     const uint32_t nt = n_tiles_of(r.n, cell_sparse::kTile);
     a.tile_meta = (const uint64_t*)(ws + L.tmeta);
-    k_tile_bounds<cell_sparse><<<(nt + 7) / 8, 256, 0, r.s>>>(S, r.n, c->dt, nt, kWSortTile, (uint64_t*)(ws + L.tmeta),
+    k_tile_bounds<cell_sparse><<<(nt + 7) / 8, 256, 0, r.s>>>(S, r.n, c->dt, nt, r.sort_T, (uint64_t*)(ws + L.tmeta),
                                                              hdr);
     TPX_LAUNCHED(c);
     k_tile_cell<cell_sparse><<<nt, cell_sparse::kThreads, cell_smem_bytes<cell_sparse>(), r.s>>>(a);
@@ -647,7 +648,6 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   r.s = (cudaStream_t)stream;
   srec* S = (srec*)(r.ws + r.L.S);
   dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
-  const uint32_t sort_tiles = n_tiles_of(n, kWSortTile);
 
   int rc;
   // attempt 0: D = 1024, attempt 1: D = 3072, attempt 2: global radix sort;
@@ -657,16 +657,20 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {
-      k_window_sort<12><<<sort_tiles, kWSortThreads, window_sort_smem<12>(), r.s>>>(hits, n, c->width, c->height, S,
-                                                                                   hdr);
+      r.sort_T = kSortT0;
+      const uint32_t sort_tiles = n_tiles_of(n, kSortT0);
+      k_window_sort<20, kSortT0><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
+                                                                                            c->height, S, hdr);
       TPX_LAUNCHED(c);
-      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kWSortTile, hdr);
+      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortT0, hdr);
       TPX_LAUNCHED(c);
     } else if (attempt == 1) {
-      k_window_sort<20><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width, c->height, S,
-                                                                                   hdr);
+      r.sort_T = kSortT1;
+      const uint32_t sort_tiles = n_tiles_of(n, kSortT1);
+      k_window_sort<20, kSortT1><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
+                                                                                            c->height, S, hdr);
       TPX_LAUNCHED(c);
-      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kWSortTile, hdr);
+      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortT1, hdr);
       TPX_LAUNCHED(c);
     } else {
       if ((rc = sort_global(c, r))) return rc;
