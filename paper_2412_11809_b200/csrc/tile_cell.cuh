@@ -75,7 +75,12 @@ struct cell_smem {
   static constexpr size_t accG = accF + kA * 4;                        // last owned local idx
   static constexpr size_t acc_end = accG + kA * 4;
   static constexpr size_t heads_end = (size_t)C::kCells * 2;
-  static constexpr size_t region_a = acc_end > heads_end ? acc_end : heads_end;
+  // edge owners during the search (u8 lane per buffered edge, one array of
+  // 32 * kEdgeBuf per warp), after the heads in region A
+  static constexpr size_t owner = heads_end;
+  static constexpr size_t owner_end = owner + (size_t)(C::kThreads / 32) * 32 * kEdgeBuf;
+  static constexpr size_t region_a0 = acc_end > heads_end ? acc_end : heads_end;
+  static constexpr size_t region_a = region_a0 > owner_end ? region_a0 : owner_end;
   static constexpr size_t rec = region_a;                              // uint2 [kM] (toa - base, y<<16|x)
   static constexpr size_t par = rec + kM * 8;                          // u32 [kM]
   static constexpr size_t nxt = par + kM * 4;                          // u16 [kM]
@@ -201,6 +206,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(smem_raw));
   auto sp = [&](size_t off) { return __cvta_shared_to_generic(sbase + (uint32_t)off); };
   uint16_t* heads = reinterpret_cast<uint16_t*>(sp(SL::heads));
+  uint8_t* owner = reinterpret_cast<uint8_t*>(sp(SL::owner)) + (threadIdx.x >> 5) * (32 * kEdgeBuf);
   uint32_t* accN = reinterpret_cast<uint32_t*>(sp(SL::accN));
   uint32_t* accT = reinterpret_cast<uint32_t*>(sp(SL::accT));
   uint32_t* accX = reinterpret_cast<uint32_t*>(sp(SL::accX));
@@ -409,9 +415,29 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         }
         hflag[j] = fl;
       }
-      __syncwarp();
-      // unions of the buffered edges (larger root under smaller)
-      for (uint32_t k = 0; k < ne; ++k) s_unite(par, j, eb[k * kTh + threadIdx.x]);
+      // unions of the buffered edges (larger root under smaller), spread over
+      // the warp: edge e of the warp's E goes to lane e % 32, so a round
+      // keeps every lane busy instead of iterating max(ne) times with the
+      // lanes that have few edges idle
+      {
+        uint32_t pre = ne;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, pre, o);
+          if (lane >= (unsigned)o) pre += y;
+        }
+        const uint32_t E = __shfl_sync(kFull, pre, 31);
+        pre -= ne;
+        for (uint32_t k = 0; k < ne; ++k) owner[pre + k] = (uint8_t)lane;
+        __syncwarp();
+        const uint32_t wbase = threadIdx.x & ~31u;
+        for (uint32_t b = 0; b < E; b += 32) {
+          const uint32_t e = b + lane;
+          const uint32_t L = e < E ? owner[e] : 0u;
+          const uint32_t pL = __shfl_sync(kFull, pre, L);
+          if (e < E) s_unite(par, chunk * 32 + L, eb[(e - pL) * kTh + wbase + L]);
+        }
+      }
       __syncwarp();
     }
   }
