@@ -215,6 +215,7 @@ struct tile_smem_buckets {
   static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2;
   static constexpr size_t ccur = eb;                                    // u32   [kTile]   (alias)
   static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
+  static_assert((size_t)kTileThreads * kEdgeBuf <= (size_t)kTile * 4, "edge owners alias crank + coff");
   static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
   static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
   static constexpr size_t eslot = hflag + kTile;                       // u16   [kFwdMax] (dense staging)
@@ -248,6 +249,7 @@ struct tile_smem_hash {
   static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2;
   static constexpr size_t ccur = eb;                                    // u32   [kTile]   (alias)
   static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
+  static_assert((size_t)kTileThreads * kEdgeBuf <= (size_t)kTile * 4, "edge owners alias crank + coff");
   static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
   static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
   static constexpr size_t total = hflag + kTile;
@@ -756,8 +758,29 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       }
       hflag[j] = fl;
     }
-    __syncwarp();
-    for (uint32_t e = 0; e < ne; ++e) s_unite(par, j, eb[e * kTileThreads + threadIdx.x]);
+    // unions of the buffered edges, spread over the warp (edge e of the
+    // warp's E to lane e % 32; owner lanes in crank/coff, unused until the
+    // compaction)
+    {
+      uint32_t pre = ne;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, pre, o);
+        if (lane >= (unsigned)o) pre += y;
+      }
+      const uint32_t E = __shfl_sync(kFull, pre, 31);
+      pre -= ne;
+      uint8_t* owner = reinterpret_cast<uint8_t*>(crank) + (threadIdx.x >> 5) * (32 * kEdgeBuf);
+      for (uint32_t k = 0; k < ne; ++k) owner[pre + k] = (uint8_t)lane;
+      __syncwarp();
+      const uint32_t wbase = threadIdx.x & ~31u;
+      for (uint32_t b = 0; b < E; b += 32) {
+        const uint32_t e = b + lane;
+        const uint32_t L = e < E ? owner[e] : 0u;
+        const uint32_t pL = __shfl_sync(kFull, pre, L);
+        if (e < E) s_unite(par, chunk * 32 + L, eb[(e - pL) * kTileThreads + wbase + L]);
+      }
+    }
     __syncwarp();
   }
   __syncthreads();
