@@ -123,6 +123,12 @@ __device__ __forceinline__ uint32_t s_find(volatile uint32_t* par, uint32_t x) {
 }
 
 __device__ __forceinline__ void s_unite(uint32_t* par, uint32_t a, uint32_t b) {
+  // start one level up: an edge inside an already-merged component (most
+  // edges of a compact cluster once its first edges are united) usually has
+  // both ends under the same parent and costs two loads
+  a = reinterpret_cast<volatile uint32_t*>(par)[a];
+  b = reinterpret_cast<volatile uint32_t*>(par)[b];
+  if (a == b) return;
   a = s_find(par, a);
   b = s_find(par, b);
   while (a != b) {
