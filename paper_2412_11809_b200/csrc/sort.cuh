@@ -139,6 +139,108 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const tpx_hit* 
   }
 }
 
+// Stable scatter for 32-bit keys, ranked in shared memory: the tile's 4096
+// elements are ranked by digit with warp-private counters (warp w owns tile
+// positions [512 w, 512 w + 512), so (warp, round, lane) order is index
+// order), placed digit-sorted in shared memory, and written out in that
+// order -- runs of equal digits go to consecutive global positions, so the
+// stores coalesce, and the tile needs four barriers instead of three per
+// 256 elements.
+template <bool kFromHits>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter_tile(const tpx_hit* __restrict__ hits,
+                                                                     const uint32_t* __restrict__ keys_in,
+                                                                     const uint32_t* __restrict__ vals_in,
+                                                                     uint64_t n, uint64_t toa_min, int shift,
+                                                                     const uint32_t* __restrict__ offsets,
+                                                                     uint32_t n_tiles, uint32_t* __restrict__ keys_out,
+                                                                     uint32_t* __restrict__ vals_out) {
+  constexpr int kWarps = kRadixThreads / 32;
+  constexpr int kPerWarp = kRadixItems * 32;
+  static_assert(kRadixThreads == kRadixBins, "one scan thread per digit");
+  __shared__ uint32_t skey[kRadixTile];
+  __shared__ uint32_t sval[kRadixTile];
+  __shared__ uint32_t wc[kWarps * kRadixBins];  // warp-major digit counters, then offsets
+  __shared__ uint32_t gb[kRadixBins];           // global position - tile-local position, by digit
+  __shared__ uint32_t dsum[kWarps];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t tbase = (uint64_t)blockIdx.x * kRadixTile;
+  const uint32_t m = (uint32_t)min((uint64_t)kRadixTile, n - tbase);
+  for (int i = threadIdx.x; i < kWarps * kRadixBins; i += kRadixThreads) wc[i] = 0;
+  uint32_t key[kRadixItems], val[kRadixItems], rk[kRadixItems];
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const uint32_t p = warp * kPerWarp + r * 32 + lane;
+    key[r] = 0;
+    val[r] = 0;
+    if (p < m) {
+      const uint64_t i = tbase + p;
+      if constexpr (kFromHits) {
+        key[r] = (uint32_t)(load_hit(hits + i).toa - toa_min);
+        val[r] = (uint32_t)i;
+      } else {
+        key[r] = keys_in[i];
+        val[r] = vals_in[i];
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* w = wc + warp * kRadixBins;
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const uint32_t p = warp * kPerWarp + r * 32 + lane;
+    const bool valid = p < m;
+    const unsigned d = valid ? (key[r] >> shift) & 0xffu : 256u;
+    const unsigned peers = __match_any_sync(kFull, d);
+    uint32_t b = 0;
+    if (valid) b = w[d];
+    rk[r] = b + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == (int)lane) w[d] = b + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const unsigned d = threadIdx.x;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kWarps; ++w2) tot += wc[w2 * kRadixBins + d];
+    uint32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) dsum[warp] = x;
+    __syncthreads();
+    uint32_t start = x - tot;
+    for (unsigned w2 = 0; w2 < warp; ++w2) start += dsum[w2];
+    gb[d] = offsets[(uint64_t)d * n_tiles + blockIdx.x] - start;
+#pragma unroll
+    for (int w2 = 0; w2 < kWarps; ++w2) {
+      const uint32_t c = wc[w2 * kRadixBins + d];
+      wc[w2 * kRadixBins + d] = start;
+      start += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const uint32_t p = warp * kPerWarp + r * 32 + lane;
+    if (p < m) {
+      const uint32_t q = w[(key[r] >> shift) & 0xffu] + rk[r];
+      skey[q] = key[r];
+      sval[q] = val[r];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < m; i += kRadixThreads) {
+    const uint32_t k = skey[i];
+    const uint32_t pos = gb[(k >> shift) & 0xffu] + i;
+    keys_out[pos] = k;
+    vals_out[pos] = sval[i];
+  }
+}
+
 // Sorted records + union-find init: rec[i] = hit[perm[i]], parent[i] = i.
 __global__ void k_gather_init(const tpx_hit* __restrict__ hits, const uint32_t* __restrict__ perm, uint64_t n,
                               srec* __restrict__ rec, uint32_t* __restrict__ parent) {

@@ -194,7 +194,15 @@ static int radix_sort(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t 
     TPX_LAUNCHED(c);
     int rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s);
     if (rc) return rc;
-    if (p == 0) {
+    if constexpr (sizeof(KeyT) == 4) {
+      if (p == 0) {
+        k_radix_scatter_tile<true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, shift, hist,
+                                                                   tiles, k1, v1);
+      } else {
+        k_radix_scatter_tile<false><<<tiles, kRadixThreads, 0, s>>>(hits, k0, v0, n, toa_min, shift, hist, tiles,
+                                                                    k1, v1);
+      }
+    } else if (p == 0) {
       k_radix_scatter<KeyT, true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, shift, hist,
                                                                   tiles, k1, v1);
     } else {
@@ -763,8 +771,7 @@ static int group_radix(tpx_cluster* c, uint64_t n, uint64_t k, uint32_t* k0, uin
     k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, shift, hist, tiles);
     TPX_LAUNCHED(c);
     if ((rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s))) return rc;
-    k_radix_scatter<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, shift, hist, tiles, k1,
-                                                                      vout);
+    k_radix_scatter_tile<false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, shift, hist, tiles, k1, vout);
     TPX_LAUNCHED(c);
     uint32_t* t = k0;
     k0 = k1;
@@ -972,8 +979,8 @@ int sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, uint32_t* tk, uint32_t*
     TPX_K(k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, 8 * p, hist, tiles));
     int rc = scan_u32(hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s);
     if (rc) return rc;
-    TPX_K(k_radix_scatter<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, 8 * p, hist, tiles,
-                                                                        k1, v1));
+    TPX_K(k_radix_scatter_tile<false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, 8 * p, hist, tiles, k1,
+                                                                     v1));
     uint32_t* t = k0;
     k0 = k1;
     k1 = t;
