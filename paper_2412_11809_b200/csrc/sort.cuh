@@ -55,6 +55,12 @@ constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 keys per tile
 constexpr int kRadixBins = 256;
+#ifndef TPX_RSCAT_MINB
+#define TPX_RSCAT_MINB 3  // resident CTAs per SM of k_radix_scatter_tile
+#endif
+#ifndef TPX_RSCAT_MINB
+#define TPX_RSCAT_MINB 3
+#endif
 
 template <typename KeyT, bool kFromHits>
 __device__ __forceinline__ KeyT radix_key(const tpx_hit* hits, const KeyT* keys, uint64_t i, uint64_t toa_min) {
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const tpx_hit* 
 // stores coalesce, and the tile needs four barriers instead of three per
 // 256 elements.
 template <bool kFromHits>
-__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter_tile(const tpx_hit* __restrict__ hits,
+__global__ void __launch_bounds__(kRadixThreads, TPX_RSCAT_MINB) k_radix_scatter_tile(const tpx_hit* __restrict__ hits,
                                                                      const uint32_t* __restrict__ keys_in,
                                                                      const uint32_t* __restrict__ vals_in,
                                                                      uint64_t n, uint64_t toa_min, int shift,
