@@ -81,11 +81,16 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const tpx_hit* __r
   h[threadIdx.x] = 0;
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * kRadixTile;
-#pragma unroll 4
+  // all digits first (16 independent loads in flight per thread), then the counting
+  unsigned dg[kRadixItems];
+#pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     uint64_t i = base + (uint64_t)r * kRadixThreads + threadIdx.x;
-    unsigned d = 256;
-    if (i < n) d = (unsigned)((radix_key<KeyT, kFromHits>(hits, keys, i, toa_min) >> shift) & 0xffu);
+    dg[r] = i < n ? (unsigned)((radix_key<KeyT, kFromHits>(hits, keys, i, toa_min) >> shift) & 0xffu) : 256u;
+  }
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const unsigned d = dg[r];
     unsigned peers = __match_any_sync(kFull, d);
     if (d < 256 && (__ffs(peers) - 1) == (int)lane_id()) atomicAdd(&h[d], (uint32_t)__popc(peers));
   }
@@ -248,18 +253,35 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_RSCAT_MINB) k_radix_scatter
 }
 
 // Sorted records + union-find init: rec[i] = hit[perm[i]], parent[i] = i.
+// Four elements per thread and iteration: the permutation loads, then the
+// dependent hit gathers, are issued together (memory-level parallelism).
 __global__ void k_gather_init(const tpx_hit* __restrict__ hits, const uint32_t* __restrict__ perm, uint64_t n,
                               srec* __restrict__ rec, uint32_t* __restrict__ parent) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t j = perm ? perm[i] : (uint32_t)i;
-    hit4 h = load_hit(hits + j);
-    srec r;
-    r.tt = (h.toa << 16) | h.tot;
-    r.xy = (h.y << 16) | h.x;
-    r.idx = j;
-    store_srec(rec + i, r);
-    parent[i] = (uint32_t)i;
+  constexpr int U = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
+    uint32_t j[U];
+    hit4 h[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      j[u] = i < n ? (perm ? perm[i] : (uint32_t)i) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) h[u] = load_hit(hits + j[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < n) {
+        srec r;
+        r.tt = (h[u].toa << 16) | h[u].tot;
+        r.xy = (h[u].y << 16) | h[u].x;
+        r.idx = j[u];
+        store_srec(rec + i, r);
+        parent[i] = (uint32_t)i;
+      }
+    }
   }
 }
 
