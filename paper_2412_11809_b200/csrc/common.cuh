@@ -111,4 +111,21 @@ __device__ __forceinline__ void uf_unite(uint32_t* parent, uint32_t a, uint32_t 
   }
 }
 
+// Small device -> host read-backs (run header, counts, probe samples) are
+// stored by a one-block kernel into mapped pinned memory instead of a
+// cudaMemcpyAsync: a D2H copy would queue on the copy engine behind whatever
+// bulk D2H another buffer has in flight (the host-buffer pipeline and the
+// streaming path overlap exactly those), stalling this run until it drains.
+__global__ void k_readback(const unsigned char* __restrict__ src, unsigned char* dst, uint32_t bytes) {
+  for (uint32_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+// host_mapped: memory from cudaHostAlloc(..., cudaHostAllocMapped)
+inline cudaError_t readback_async(void* host_mapped, const void* dev, size_t bytes, cudaStream_t s) {
+  void* dptr = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&dptr, host_mapped, 0);
+  if (e != cudaSuccess) return e;
+  k_readback<<<1, 256, 0, s>>>((const unsigned char*)dev, (unsigned char*)dptr, (uint32_t)bytes);
+  return cudaGetLastError();
+}
+
 }  // namespace tpx

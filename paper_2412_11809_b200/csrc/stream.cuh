@@ -373,7 +373,8 @@ static int stream_pass(stream_dev* d, const tpx_hit* fresh, const uint64_t* fres
   if ((rc = exclusive_scan(c, d->d_open, n, d->d_cpos, d->d_partials, d->d_counts + 2, st))) return rc;
   k_stream_carry<<<gn, 256, 0, st>>>(hits, gidx, n, d->d_open, d->d_cpos, d->d_carry, d->d_carry_g);
   TPX_LAUNCHED(c);
-  TPX_CUDA(cudaMemcpyAsync(d->h_counts, d->d_counts, 12, cudaMemcpyDeviceToHost, st));
+  TPX_CUDA(readback_async(d->h_counts, d->d_counts, 12, st));
+  c->stats.kernel_launches++;
   TPX_CUDA(cudaStreamSynchronize(st));
   *kc_out = d->h_counts[0];
   *nh_out = d->h_counts[1];
@@ -546,7 +547,7 @@ int tpx_stream_create(const tpx_stream_config* cfg, void* workspace, size_t work
   s->d_out_cl = (tpx_stream_cluster*)(w + L.out_cl);
   tpx::stream_dev_bind(&s->dev, w, L.dev, workspace_bytes);
   if (cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess ||
-      cudaMallocHost(&s->dev.h_counts, 64) != cudaSuccess || !s->bf.buf.reserve(1024) || !s->bf.next.reserve(1024) ||
+      cudaHostAlloc((void**)&s->dev.h_counts, 64, cudaHostAllocMapped) != cudaSuccess || !s->bf.buf.reserve(1024) || !s->bf.next.reserve(1024) ||
       !s->bf.buf_g.reserve(1024) || !s->bf.next_g.reserve(1024)) {
     tpx_stream_destroy(s);
     return TPX_ERR_CUDA;

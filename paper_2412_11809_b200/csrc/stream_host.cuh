@@ -14,6 +14,9 @@
 // those of tpx_stream_push/flush (same BufFill decisions, same carry).
 #pragma once
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace tpx {
 
@@ -175,8 +178,8 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
   TPX_RH(cudaEventCreateWithFlags(&e_done, cudaEventDisableTiming));
   TPX_RH(cudaEventCreate(&t0));
   TPX_RH(cudaEventCreate(&t1));
-  TPX_RH(cudaMallocHost(&d.h_counts, 64));
-  TPX_RH(cudaMallocHost(&h_scan, 64));
+  TPX_RH(cudaHostAlloc((void**)&d.h_counts, 64, cudaHostAllocMapped));
+  TPX_RH(cudaHostAlloc((void**)&h_scan, 64, cudaHostAllocMapped));
   TPX_RH(cudaEventRecord(t0, d.s));
 
   // issue the H2D of a plan's moved hits and run (the run straight from the
@@ -197,7 +200,7 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
       k_run_scan<<<grid_for(rl, 256), 256, 0, s_h2d>>>(d_new[sl] + p.m0, rl, cut_before, have ? 1 : 0, d_scan[sl]);
       if (cudaGetLastError() != cudaSuccess) return TPX_ERR_CUDA;
     }
-    if (cudaMemcpyAsync(h_scan + 2 * sl, d_scan[sl], 16, cudaMemcpyDeviceToHost, s_h2d) != cudaSuccess ||
+    if (readback_async(h_scan + 2 * sl, d_scan[sl], 16, s_h2d) != cudaSuccess ||
         cudaEventRecord(e_scan[sl], s_h2d) != cudaSuccess)
       return TPX_ERR_CUDA;
     return TPX_OK;
@@ -279,6 +282,10 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
     return rc;
   }
   bool use_prev_out[2] = {false, false};
+  const bool trace = getenv("TPX_STREAM_TRACE") != nullptr;
+  double tr[5] = {0, 0, 0, 0, 0};  // issue_run, stream_pass, d2h issue, take_scan, route
+  auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double ta = now();
   for (;;) {
     const int sl = cur.slot;
     // the next buffer's run goes out now (overlaps this buffer's kernels),
@@ -289,6 +296,7 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
       nxt = plan_after(cur);
       if ((rc = issue_run(nxt, cur.cut, true))) break;
     }
+    if (trace) { double tb = now(); tr[0] += tb - ta; ta = tb; }
     // cluster this buffer
     if (cudaStreamWaitEvent(d.s, e_in[sl], 0) != cudaSuccess) {
       rc = TPX_ERR_CUDA;
@@ -302,6 +310,7 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
     stream_out out{d_out_cl[sl], nullptr, nullptr, d_out_g32[sl], h_total};
     uint64_t kc = 0, nh = 0;
     if ((rc = stream_pass(&d, d_new[sl], d_new_g[sl], nn, cur.cut, cur.final_buffer, out, &kc, &nh))) break;
+    if (trace) { double tb = now(); tr[1] += tb - ta; ta = tb; }
     // drain the results on the D2H stream
     if (cudaEventRecord(e_done, d.s) != cudaSuccess || cudaStreamWaitEvent(s_d2h, e_done, 0) != cudaSuccess) {
       rc = TPX_ERR_CUDA;
@@ -323,6 +332,7 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
       break;
     }
     use_prev_out[sl] = true;
+    if (trace) { double tb = now(); tr[2] += tb - ta; ta = tb; }
     k_total += kc;
     h_total += nh;
     st.buffers++;
@@ -332,9 +342,14 @@ int tpx_stream_run_host(const tpx_stream_config* cfg, const tpx_hit* hits, uint6
     last_cut = cur.cut;
     have_cut = true;
     if ((rc = take_scan(nxt.slot))) break;
+    if (trace) { double tb = now(); tr[3] += tb - ta; ta = tb; }
     cur = nxt;
     if ((rc = route(cur))) break;
+    if (trace) { double tb = now(); tr[4] += tb - ta; ta = tb; }
   }
+  if (trace)
+    fprintf(stderr, "stream trace (ms): issue_run %.2f stream_pass %.2f d2h_issue %.2f take_scan %.2f route %.2f buffers %llu\n",
+            tr[0], tr[1], tr[2], tr[3], tr[4], (unsigned long long)st.buffers);
 #undef TPX_RH
   if (rc == TPX_OK) {
     if (cudaEventRecord(t1, s_d2h) != cudaSuccess || cudaEventSynchronize(t1) != cudaSuccess) rc = TPX_ERR_CUDA;

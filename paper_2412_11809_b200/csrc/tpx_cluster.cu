@@ -88,11 +88,14 @@ layout make_layout(uint64_t n) {
 
 }  // namespace
 
+constexpr size_t kHostMapBytes = 4096;  // mapped pinned read-back area per context
+
 struct tpx_cluster {
   uint64_t dt;
   int variant;
   uint32_t width, height;
-  dev_hdr* host_hdr;  // pinned
+  dev_hdr* host_hdr;  // mapped pinned, 4 KB: the header, then scratch for other read-backs
+  char* host_scratch;
   int profiling;
   int tile_mode;  // TPX_TILE_*
   cudaEvent_t ev[kMaxStages + 1];
@@ -143,7 +146,8 @@ static int ensure_cuda(tpx_cluster* c) {
       cudaFuncSetAttribute(k_tile_cell<cell_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)cell_smem_bytes<cell_sparse>()) != cudaSuccess)
     return TPX_ERR_CUDA;
-  if (cudaMallocHost(&c->host_hdr, sizeof(dev_hdr)) != cudaSuccess) return TPX_ERR_CUDA;
+  if (cudaHostAlloc((void**)&c->host_hdr, kHostMapBytes, cudaHostAllocMapped) != cudaSuccess) return TPX_ERR_CUDA;
+  c->host_scratch = reinterpret_cast<char*>(c->host_hdr) + sizeof(dev_hdr);
   for (int i = 0; i <= kMaxStages; ++i) {
     if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
       for (int k = 0; k < i; ++k) cudaEventDestroy(c->ev[k]);
@@ -247,8 +251,19 @@ static int reset_header(tpx_cluster* c, const run_ptrs& r) {
 }
 
 static int read_header(tpx_cluster* c, const run_ptrs& r) {
-  TPX_CUDA(cudaMemcpyAsync(c->host_hdr, r.ws + r.L.hdr, sizeof(dev_hdr), cudaMemcpyDeviceToHost, r.s));
+  TPX_CUDA(readback_async(c->host_hdr, r.ws + r.L.hdr, sizeof(dev_hdr), r.s));
+  c->stats.kernel_launches++;
   TPX_CUDA(cudaStreamSynchronize(r.s));
+  return TPX_OK;
+}
+
+// Small read-back into a host variable through the context's mapped scratch.
+static int readback_sync(tpx_cluster* c, void* dst, const void* dev, size_t bytes, cudaStream_t s) {
+  if (bytes > kHostMapBytes - sizeof(dev_hdr)) return TPX_ERR_INVALID_ARG;
+  TPX_CUDA(readback_async(c->host_scratch, dev, bytes, s));
+  c->stats.kernel_launches++;
+  TPX_CUDA(cudaStreamSynchronize(s));
+  memcpy(dst, c->host_scratch, bytes);
   return TPX_OK;
 }
 
@@ -505,8 +520,7 @@ static int run_variant(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t
     TPX_LAUNCHED(c);
     if (c->variant == TPX_VARIANT_GLOBAL) {
       unsigned long long span = 0;
-      TPX_CUDA(cudaMemcpyAsync(&span, d_span, 8, cudaMemcpyDeviceToHost, s));
-      TPX_CUDA(cudaStreamSynchronize(s));
+      if ((rc = readback_sync(c, &span, d_span, 8, s))) return rc;
       if (span + dt > W) {  // a candidate older than W might have been missed
         const uint64_t grow = 2 * (span + dt) + 64;
         W = grow > 4 * W ? grow : 4 * W;
@@ -532,8 +546,7 @@ static int run_variant(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t
     TPX_LAUNCHED(c);
   }
   uint32_t k = 0;
-  TPX_CUDA(cudaMemcpyAsync(&k, ws + V.misc + 64, 4, cudaMemcpyDeviceToHost, s));
-  TPX_CUDA(cudaStreamSynchronize(s));
+  if ((rc = readback_sync(c, &k, ws + V.misc + 64, 4, s))) return rc;
   *n_clusters_out = k;
   c->stats.n_clusters = k;
   c->stats.cross_pairs = W;  // diagnostics: final island window (ticks)
@@ -695,9 +708,11 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       if (probe_on) {
         k_density_probe<<<1, kProbeSamples, 0, r.s>>>(S, n, c->dt, probe);
         TPX_LAUNCHED(c);
-        TPX_CUDA(cudaMemcpyAsync(hprobe, probe, sizeof(hprobe), cudaMemcpyDeviceToHost, r.s));
+        TPX_CUDA(readback_async(c->host_scratch, probe, sizeof(hprobe), r.s));
+        c->stats.kernel_launches++;
       }
-      if ((rc = read_header(c, r))) return rc;
+      if ((rc = read_header(c, r))) return rc;  // synchronises the stream: the probe samples are in as well
+      if (probe_on) memcpy(hprobe, c->host_scratch, sizeof(hprobe));
       if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
       if (attempt < 2 && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
         c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
@@ -874,8 +889,7 @@ int tpx_cluster_run_grouped(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       TPX_LAUNCHED(c);
     }
     unsigned int bad = 0;
-    TPX_CUDA(cudaMemcpyAsync(&bad, &hdr->sort_bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
-    TPX_CUDA(cudaStreamSynchronize(s));
+    if ((rc = readback_sync(c, &bad, &hdr->sort_bad, sizeof(bad), s))) return rc;
     if (bad) {
       c->stats.sort_retries += 1;
       k_group_keys<<<gn, 256, 0, s>>>(S, n, cpos, grank, k0, v0);
