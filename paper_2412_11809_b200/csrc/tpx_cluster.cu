@@ -240,13 +240,20 @@ struct run_ptrs {
   bool column;  // legacy column-bucket sparse kernel (TPX_TILE_COLUMN, comparison only)
 };
 
+// The header is initialised by a kernel, not by an H2D copy of a host
+// struct: with several buffers in flight (tpx_pipeline, the streaming path)
+// a small H2D would queue on the copy engine behind another buffer's bulk
+// H2D and hold this run until it drained.
+__global__ void k_reset_hdr(dev_hdr* h) {
+  static_assert(sizeof(dev_hdr) % 8 == 0 && offsetof(dev_hdr, toa_min) == 0, "header layout");
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(h);
+  for (uint32_t i = threadIdx.x; i < sizeof(dev_hdr) / 8; i += blockDim.x) w[i] = i == 0 ? ~0ull : 0ull;
+}
+
 static int reset_header(tpx_cluster* c, const run_ptrs& r) {
-  dev_hdr init;
-  memset(&init, 0, sizeof(init));
-  init.toa_min = ~0ull;
-  TPX_CUDA(cudaMemcpyAsync(r.ws + r.L.hdr, &init, sizeof(init), cudaMemcpyHostToDevice, r.s));
+  k_reset_hdr<<<1, 32, 0, r.s>>>((dev_hdr*)(r.ws + r.L.hdr));
+  TPX_LAUNCHED(c);
   TPX_CUDA(cudaMemsetAsync(r.ws + r.L.bitmap, 0, (size_t)r.L.nwords * 4, r.s));
-  (void)c;
   return TPX_OK;
 }
 
