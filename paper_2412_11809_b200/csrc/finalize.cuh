@@ -53,9 +53,31 @@ __global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __
 __global__ void __launch_bounds__(kListThreads) k_flatten_open(const uint32_t* __restrict__ open_hits, dev_hdr* hdr,
                                                                uint32_t* parent_g) {
   const uint64_t nh = hdr->n_open_hits;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t pos = open_hits[t];
-    parent_g[pos] = uf_root(parent_g, pos);
+  // 4 hits per thread and iteration: their dependent root walks overlap
+  constexpr int U = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < nh; t0 += U * stride) {
+    uint32_t pos[U], cur[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) pos[u] = t0 + u * stride < nh ? open_hits[t0 + u * stride] : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = pos[u] != 0xffffffffu ? ld_cg(parent_g + pos[u]) : 0u;
+    // the four root walks advance in lock step (one round = up to 4 loads)
+    for (bool more = true; more;) {
+      more = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (pos[u] == 0xffffffffu) continue;
+        const uint32_t nx = ld_cg(parent_g + cur[u]);
+        if (nx != cur[u]) {
+          cur[u] = nx;
+          more = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (pos[u] != 0xffffffffu) parent_g[pos[u]] = cur[u];
   }
 }
 
@@ -109,9 +131,20 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
                                                               uint32_t n_owned, uint32_t* __restrict__ first_of_label) {
   const uint64_t nh = hdr->n_open_hits, nc = hdr->n_open_comps;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh; t += stride) {
-    const uint32_t pos = open_hits[t];
-    labels[S[pos].idx] = stage[slot_of[parent_g[pos]]].label;  // flattened
+  constexpr int U = 4;  // 4 dependent load chains in flight per thread
+  for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < nh; t0 += U * stride) {
+    uint32_t pos[U], idx[U], lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) pos[u] = t0 + u * stride < nh ? open_hits[t0 + u * stride] : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (pos[u] != 0xffffffffu) {
+        idx[u] = S[pos[u]].idx;
+        lab[u] = stage[slot_of[parent_g[pos[u]]]].label;  // flattened
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (pos[u] != 0xffffffffu) labels[idx[u]] = lab[u];
   }
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += stride) {
     const uint32_t r = open_comps[t];
