@@ -505,8 +505,13 @@ static int run_variant(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t
     k_fill_iota32<<<gn, 256, 0, s>>>(par, n);
     TPX_LAUNCHED(c);
     TPX_CUDA(cudaMemsetAsync(stamp, 0, n * 4, s));
+    // the island features are not needed past the grouped run: their space
+    // holds the hits gathered in island order
+    tpx_hit* ih = (tpx_hit*)(ws + V.feats);
+    k_gather_hits<<<gn, 256, 0, s>>>(hits, order, n, ih);
+    TPX_LAUNCHED(c);
     variant_args a;
-    a.hits = hits;
+    a.ih = ih;
     a.order = order;
     a.offsets = offsets;
     a.k = k_is;

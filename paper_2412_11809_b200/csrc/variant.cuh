@@ -27,7 +27,7 @@
 namespace tpx {
 
 struct variant_args {
-  const tpx_hit* hits;
+  const tpx_hit* ih;        // hits gathered in grouped order (ih[p] = hits[order[p]])
   const uint32_t* order;    // grouped order: input index per position
   const uint32_t* offsets;  // island blocks
   uint64_t k;               // islands
@@ -61,17 +61,25 @@ __device__ __forceinline__ bool var_adjacent(const hit4& p, const hit4& q) {
   return dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1;
 }
 
+// Hits in grouped (island) order, so the window scans below read contiguous
+// records instead of a dependent order -> hit gather per candidate.
+__global__ void k_gather_hits(const tpx_hit* __restrict__ hits, const uint32_t* __restrict__ order, uint64_t n,
+                              tpx_hit* __restrict__ out) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+    out[p] = hits[order[p]];
+}
+
 // Small islands: one thread runs the process over the island's hits.
 __global__ void k_variant_small(variant_args a) {
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.k; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t o0 = a.offsets[g], o1 = a.offsets[g + 1];
     if (o1 - o0 >= kVarWarpMin) continue;
     for (uint32_t p = o0; p < o1; ++p) {
-      const hit4 hi = load_hit(a.hits + a.order[p]);
+      const hit4 hi = load_hit(a.ih + p);
       const uint64_t ti = hi.toa;
       // pass 1: mark the roots that may take the hit (states before merging)
       for (uint32_t q = p; q-- > o0;) {
-        const hit4 hq = load_hit(a.hits + a.order[q]);
+        const hit4 hq = load_hit(a.ih + q);
         if (hq.toa + a.window < ti) break;
         if (!var_adjacent(hi, hq)) continue;
         const uint32_t r = var_find(a.par, q);
@@ -81,7 +89,7 @@ __global__ void k_variant_small(variant_args a) {
       uint32_t target = 0xffffffffu;
       unsigned long long mn = ti, mx = ti;
       for (uint32_t q = p; q-- > o0;) {
-        const hit4 hq = load_hit(a.hits + a.order[q]);
+        const hit4 hq = load_hit(a.ih + q);
         if (hq.toa + a.window < ti) break;
         if (!var_adjacent(hi, hq)) continue;
         const uint32_t r = var_find(a.par, q);
@@ -117,14 +125,14 @@ __global__ void k_variant_large(variant_args a) {
       todo &= todo - 1;
       const uint32_t o0 = a.offsets[g], o1 = a.offsets[g + 1];
       for (uint32_t p = o0; p < o1; ++p) {
-        const hit4 hi = load_hit(a.hits + a.order[p]);
+        const hit4 hi = load_hit(a.ih + p);
         const uint64_t ti = hi.toa;
         // pass 1 (no linking: concurrent path halving is benign)
         for (uint32_t base = p; base > o0;) {
           const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
           bool in = false;
           if (q != 0xffffffffu && q >= o0) {
-            const hit4 hq = load_hit(a.hits + a.order[q]);
+            const hit4 hq = load_hit(a.ih + q);
             in = hq.toa + a.window >= ti;
             if (in && var_adjacent(hi, hq)) {
               const uint32_t r = var_find(a.par, q);
@@ -142,7 +150,7 @@ __global__ void k_variant_large(variant_args a) {
           const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
           bool in = false;
           if (q != 0xffffffffu && q >= o0) {
-            const hit4 hq = load_hit(a.hits + a.order[q]);
+            const hit4 hq = load_hit(a.ih + q);
             in = hq.toa + a.window >= ti;
             if (in && var_adjacent(hi, hq)) {
               uint32_t r = q;
@@ -170,7 +178,7 @@ __global__ void k_variant_large(variant_args a) {
             const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
             bool in = false;
             if (q != 0xffffffffu && q >= o0) {
-              const hit4 hq = load_hit(a.hits + a.order[q]);
+              const hit4 hq = load_hit(a.ih + q);
               in = hq.toa + a.window >= ti;
               if (in && var_adjacent(hi, hq)) {
                 uint32_t r = q;
