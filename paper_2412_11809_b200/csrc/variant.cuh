@@ -113,7 +113,11 @@ __global__ void k_variant_small(variant_args a) {
 }
 
 // Large islands: one warp per island; lanes scan the window 32 at a time.
-__global__ void k_variant_large(variant_args a) {
+constexpr uint32_t kVarAdjCap = 256;  // listed adjacent candidates per warp and hit
+
+__global__ void __launch_bounds__(256) k_variant_large(variant_args a) {
+  __shared__ uint32_t s_adj[256 / 32][kVarAdjCap];
+  uint32_t* adj = s_adj[threadIdx.x >> 5];
   const unsigned lane = lane_id();
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t g0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; g0 < a.k; g0 += nw * 32) {
@@ -127,43 +131,55 @@ __global__ void k_variant_large(variant_args a) {
       for (uint32_t p = o0; p < o1; ++p) {
         const hit4 hi = load_hit(a.ih + p);
         const uint64_t ti = hi.toa;
-        // pass 1 (no linking: concurrent path halving is benign)
+        // pass 1 (no linking: concurrent path halving is benign); the
+        // adjacent candidates are listed so passes 2 and 3 visit only them
+        uint32_t nadj = 0;
         for (uint32_t base = p; base > o0;) {
           const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
-          bool in = false;
+          bool in = false, isadj = false;
           if (q != 0xffffffffu && q >= o0) {
             const hit4 hq = load_hit(a.ih + q);
             in = hq.toa + a.window >= ti;
-            if (in && var_adjacent(hi, hq)) {
+            isadj = in && var_adjacent(hi, hq);
+            if (isadj) {
               const uint32_t r = var_find(a.par, q);
               if (var_pred(a, r, ti)) a.stamp[r] = p + 1;
             }
           }
+          const unsigned bm = __ballot_sync(kFull, isadj);
+          if (isadj && nadj + __popc(bm) <= kVarAdjCap) adj[nadj + __popc(bm & lanemask_lt())] = q;
+          nadj += __popc(bm);
           if (!__any_sync(kFull, in)) break;
           base = base > 32 ? base - 32 : 0;
         }
         __syncwarp();
+        const bool listed = nadj <= kVarAdjCap;
         // pass 2: candidate roots -> warp min (target), min/max of their spans
         uint32_t tmin = 0xffffffffu;
         unsigned long long mn = ti, mx = ti;
-        for (uint32_t base = p; base > o0;) {
-          const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
-          bool in = false;
-          if (q != 0xffffffffu && q >= o0) {
-            const hit4 hq = load_hit(a.ih + q);
-            in = hq.toa + a.window >= ti;
-            if (in && var_adjacent(hi, hq)) {
-              uint32_t r = q;
-              while (a.par[r] != r) r = a.par[r];  // read-only: no writes in this pass
-              if (a.stamp[r] == p + 1) {
-                tmin = min(tmin, r);
-                mn = min(mn, a.cmin[r]);
-                mx = max(mx, a.cmax[r]);
-              }
-            }
+        auto take = [&](uint32_t q) {
+          uint32_t r = q;
+          while (a.par[r] != r) r = a.par[r];  // read-only: no writes in this pass
+          if (a.stamp[r] == p + 1) {
+            tmin = min(tmin, r);
+            mn = min(mn, a.cmin[r]);
+            mx = max(mx, a.cmax[r]);
           }
-          if (!__any_sync(kFull, in)) break;
-          base = base > 32 ? base - 32 : 0;
+        };
+        if (listed) {
+          for (uint32_t i = lane; i < nadj; i += 32) take(adj[i]);
+        } else {
+          for (uint32_t base = p; base > o0;) {
+            const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
+            bool in = false;
+            if (q != 0xffffffffu && q >= o0) {
+              const hit4 hq = load_hit(a.ih + q);
+              in = hq.toa + a.window >= ti;
+              if (in && var_adjacent(hi, hq)) take(q);
+            }
+            if (!__any_sync(kFull, in)) break;
+            base = base > 32 ? base - 32 : 0;
+          }
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
@@ -174,20 +190,25 @@ __global__ void k_variant_large(variant_args a) {
         __syncwarp();
         // pass 3: link every candidate root under the target
         if (tmin != 0xffffffffu) {
-          for (uint32_t base = p; base > o0;) {
-            const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
-            bool in = false;
-            if (q != 0xffffffffu && q >= o0) {
-              const hit4 hq = load_hit(a.ih + q);
-              in = hq.toa + a.window >= ti;
-              if (in && var_adjacent(hi, hq)) {
-                uint32_t r = q;
-                while (a.par[r] != r && a.stamp[r] != p + 1) r = a.par[r];
-                if (a.stamp[r] == p + 1 && r != tmin) a.par[r] = tmin;  // same value from every lane
+          auto link = [&](uint32_t q) {
+            uint32_t r = q;
+            while (a.par[r] != r && a.stamp[r] != p + 1) r = a.par[r];
+            if (a.stamp[r] == p + 1 && r != tmin) a.par[r] = tmin;  // same value from every lane
+          };
+          if (listed) {
+            for (uint32_t i = lane; i < nadj; i += 32) link(adj[i]);
+          } else {
+            for (uint32_t base = p; base > o0;) {
+              const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
+              bool in = false;
+              if (q != 0xffffffffu && q >= o0) {
+                const hit4 hq = load_hit(a.ih + q);
+                in = hq.toa + a.window >= ti;
+                if (in && var_adjacent(hi, hq)) link(q);
               }
+              if (!__any_sync(kFull, in)) break;
+              base = base > 32 ? base - 32 : 0;
             }
-            if (!__any_sync(kFull, in)) break;
-            base = base > 32 ? base - 32 : 0;
           }
         }
         __syncwarp();

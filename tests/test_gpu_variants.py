@@ -76,6 +76,21 @@ def test_variant_presets(tpx, variant, preset, n):
     _check(tpx, h, tpxgen.PRESETS[preset]["dt_max"], variant, ctx=f"{variant}/{preset}")
 
 
+@pytest.mark.parametrize("variant", ["global", "static"])
+def test_variant_dense_pile(tpx, variant):
+    """A pile of hits on a 2x2 sensor inside one window: every hit has far
+    more adjacent earlier candidates than the large-island kernel lists per
+    hit (256), so its full-window fallback scan is exercised; a sparse tail
+    keeps the listed path in the same run."""
+    rng = np.random.default_rng(909)
+    dt = 16
+    pile = tpxgen.random_small(rng, 1500, 2, 2, 2 * dt)
+    tail = tpxgen.random_small(rng, 1500, 2, 2, 400 * dt)
+    tail["toa"] += np.uint64(10 * dt)
+    h = np.concatenate([pile, tail])
+    _check(tpx, h, dt, variant, 2, 2, ctx=f"{variant} dense pile")
+
+
 def test_variant_window_growth(tpx):
     # long-lived (b)-clusters: a pixel chain growing for 20 dt -> the island
     # window must grow past the first guess
