@@ -234,7 +234,12 @@ __global__ void k_variant_roots(uint32_t* __restrict__ par, const uint32_t* __re
     while (par[r] != r) r = par[r];
     root_of[p] = r;
     atomicMin(minidx + r, order[p]);
-    if (r == p) atomicMax(max_span, cmax[r] - cmin[r]);
+    if (r == p) {
+      // one address for every root: read before the atomic, so only spans
+      // above the running maximum serialise on it
+      const unsigned long long sp = cmax[r] - cmin[r];
+      if (sp > *reinterpret_cast<volatile unsigned long long*>(max_span)) atomicMax(max_span, sp);
+    }
   }
 }
 
