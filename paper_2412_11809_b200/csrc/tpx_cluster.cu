@@ -554,7 +554,8 @@ static int run_variant(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t
   if (capacity) {
     k_variant_feat_init<<<grid_for(n, 256), 256, 0, s>>>(n, rbits, rbase, features_out, capacity);
     TPX_LAUNCHED(c);
-    k_variant_feat_accum<<<grid_for(n, 256), 256, 0, s>>>(hits, n, labels_out, rbits, rbase, features_out, capacity);
+    k_variant_feat_accum_grouped<<<grid_for(n, 256), 256, 0, s>>>((const tpx_hit*)(ws + V.feats), order, n, labels_out,
+                                                                   rbits, rbase, features_out, capacity);
     TPX_LAUNCHED(c);
   }
   uint32_t k = 0;

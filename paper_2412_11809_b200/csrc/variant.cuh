@@ -266,22 +266,41 @@ __global__ void k_variant_feat_init(uint64_t n, const uint32_t* __restrict__ rbi
   }
 }
 
-__global__ void k_variant_feat_accum(const tpx_hit* __restrict__ hits, uint64_t n, const uint32_t* __restrict__ labels,
-                                     const uint32_t* __restrict__ rbits, const uint32_t* __restrict__ rbase,
-                                     tpx_cluster_features* __restrict__ feats, uint64_t capacity) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t o = bit_rank(rbits, rbase, labels[i]);
+// Feature accumulation over the hits in island order (ih[p] = hits[order[p]]):
+// positions of one record are mostly adjacent there, and within an island
+// in (toa, index) order, so lanes with the same record are reduced first
+// and one lane per group issues the atomics (ToA min / max = the group's
+// first / last lane).
+__global__ void k_variant_feat_accum_grouped(const tpx_hit* __restrict__ ih, const uint32_t* __restrict__ order,
+                                             uint64_t n, const uint32_t* __restrict__ labels,
+                                             const uint32_t* __restrict__ rbits, const uint32_t* __restrict__ rbase,
+                                             tpx_cluster_features* __restrict__ feats, uint64_t capacity) {
+  const unsigned lane = lane_id();
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned am = __activemask();
+    const uint64_t o = bit_rank(rbits, rbase, labels[order[p]]);
+    const hit4 h = load_hit(ih + p);
+    const unsigned peers = __match_any_sync(am, (unsigned)o);  // o < 2^32 (o < n)
+    const uint32_t tx = (uint32_t)h.tot * h.x, ty = (uint32_t)h.tot * h.y;  // < 2^32 each
+    const uint32_t s_tot = __reduce_add_sync(peers, (uint32_t)h.tot);
+    const uint32_t s_x = __reduce_add_sync(peers, (uint32_t)h.x);
+    const uint32_t s_y = __reduce_add_sync(peers, (uint32_t)h.y);
+    const uint64_t s_tx = (uint64_t)__reduce_add_sync(peers, tx & 0xffffu) +
+                          ((uint64_t)__reduce_add_sync(peers, tx >> 16) << 16);
+    const uint64_t s_ty = (uint64_t)__reduce_add_sync(peers, ty & 0xffffu) +
+                          ((uint64_t)__reduce_add_sync(peers, ty >> 16) << 16);
     if (o >= capacity) continue;
-    const hit4 h = load_hit(hits + i);
     tpx_cluster_features* f = feats + o;
-    atomicAdd(&f->size, 1u);
-    atomicMin((unsigned long long*)&f->toa_min, (unsigned long long)h.toa);
-    atomicMax((unsigned long long*)&f->toa_max, (unsigned long long)h.toa);
-    atomicAdd((unsigned long long*)&f->tot_sum, (unsigned long long)h.tot);
-    atomicAdd((unsigned long long*)&f->sum_x, (unsigned long long)h.x);
-    atomicAdd((unsigned long long*)&f->sum_y, (unsigned long long)h.y);
-    atomicAdd((unsigned long long*)&f->sum_tot_x, (unsigned long long)h.tot * h.x);
-    atomicAdd((unsigned long long*)&f->sum_tot_y, (unsigned long long)h.tot * h.y);
+    if ((int)lane == __ffs(peers) - 1) {
+      atomicAdd(&f->size, (uint32_t)__popc(peers));
+      atomicMin((unsigned long long*)&f->toa_min, (unsigned long long)h.toa);
+      atomicAdd((unsigned long long*)&f->tot_sum, (unsigned long long)s_tot);
+      atomicAdd((unsigned long long*)&f->sum_x, (unsigned long long)s_x);
+      atomicAdd((unsigned long long*)&f->sum_y, (unsigned long long)s_y);
+      atomicAdd((unsigned long long*)&f->sum_tot_x, (unsigned long long)s_tx);
+      atomicAdd((unsigned long long*)&f->sum_tot_y, (unsigned long long)s_ty);
+    }
+    if ((int)lane == 31 - __clz(peers)) atomicMax((unsigned long long*)&f->toa_max, (unsigned long long)h.toa);
   }
 }
 
