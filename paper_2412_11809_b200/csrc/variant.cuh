@@ -39,7 +39,10 @@ struct variant_args {
   uint32_t* stamp;          // candidate marks: stamp[root] = position + 1
 };
 
-constexpr uint32_t kVarWarpMin = 32;
+#ifndef TPX_VAR_WARP_MIN
+#define TPX_VAR_WARP_MIN 16
+#endif
+constexpr uint32_t kVarWarpMin = TPX_VAR_WARP_MIN;  // islands this large get a warp
 
 __device__ __forceinline__ uint32_t var_find(uint32_t* par, uint32_t x) {
   uint32_t p;
