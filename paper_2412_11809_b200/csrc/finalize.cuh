@@ -11,7 +11,10 @@
 namespace tpx {
 
 constexpr int kListThreads = 256;
-constexpr int kListGrid = 148 * 8;
+#ifndef TPX_LIST_GRID
+#define TPX_LIST_GRID (148 * 32)  // swept 148 x {4, 8, 16, 32}: 32 best (mixed merge + emit 1.08 -> 1.01 ms)
+#endif
+constexpr int kListGrid = TPX_LIST_GRID;
 
 __device__ __forceinline__ void flag_internal(dev_hdr* hdr) { atomicOr(&hdr->err, 2u); }
 
