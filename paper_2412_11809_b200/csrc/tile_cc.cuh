@@ -34,7 +34,10 @@ namespace tpx {
 
 constexpr int kTile = 1024;                    // smallest tile (comp_count sizing)
 constexpr int kMaxTile = 4096;                 // largest tile (stage slot sizing)
-constexpr int kBackCap = 256;                  // staged back-halo hits (openness only)
+#ifndef TPX_BACK_CAP
+#define TPX_BACK_CAP 64  // swept 64 / 128 / 256: 64 fastest on mixed, heavy-ion and Timepix4 (fewer idle loads; a truncated back halo only marks hits open)
+#endif
+constexpr int kBackCap = TPX_BACK_CAP;         // staged back-halo hits (openness only)
 constexpr int kHeadBits = 14;                  // dense pixel hash: slot word = pixel << 14 | list head
 constexpr uint32_t kHeadMask = (1u << kHeadBits) - 1;
 constexpr uint32_t kPixEmpty = 0xffffffffu >> kHeadBits;  // empty hash slot key (pixel ids must be < 2^18 - 1)
