@@ -26,9 +26,11 @@ constexpr int kWRadix = 1 << kWDigitBits;
 static_assert(kWRadix <= kWSortThreads, "one scan thread per digit");
 
 // windowed sort attempts of tpx_cluster_run: 0 -> 8192 outputs per CTA from
-// a 10240-hit window (IT = 20, D = 1024, 1.25x redundancy); 1 -> 4096 outputs
-// from the same window (D = 3072, Timepix4-rate streams)
+// a 10240-hit window (IT = 20, D = 1024, 1.25x redundancy); 1 -> 5120 outputs
+// (D = 2560, 2x: Timepix4-rate streams, displacement up to ~2300); 2 -> 4096
+// outputs (D = 3072, 2.5x)
 constexpr int kSortT0 = 8192;
+constexpr int kSortTm = 5120;
 constexpr int kSortT1 = 4096;
 
 template <int IT, int T = kWSortTile>

@@ -103,7 +103,7 @@ struct tpx_cluster {
   int cuda_ready;  // CUDA resources are created lazily by the first run
   int bitmap_valid;  // the last run left the label bitmap + its word scan in the workspace (tile path)
   int want_first;    // next run records each cluster's first sorted position (grouped runs)
-  int sort_start;  // first sort attempt (0: D=1024 window, 1: D=3072 window, 2: global radix);
+  int sort_start;  // first sort attempt (0: D=1024 window, 1: D=2560, 2: D=3072, 3: global radix);
                    // raised to the attempt that succeeded, so a stream whose disorder exceeds
                    // the window bound pays the failed attempts once, not on every run
   tpx_cluster* island;  // variants (b)/(c): (a)-context whose components are the islands
@@ -138,6 +138,8 @@ static int ensure_cuda(tpx_cluster* c) {
       cudaFuncSetAttribute(k_window_sort_kv<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_kv_smem<12>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_window_sort<20, kSortT1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)window_sort_smem<20>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_window_sort<20, kSortTm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_smem<20>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
@@ -684,10 +686,12 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
 
   int rc;
-  // attempt 0: D = 1024, attempt 1: D = 3072, attempt 2: global radix sort;
-  // attempt 3: global union-find pipeline (internal fallback)
+  // attempts 0 / 1 / 2: windowed sort with D = 1024 / 2560 / 3072;
+  // attempt 3: global radix sort; attempt 4: global union-find pipeline
+  // (internal fallback)
+  constexpr int kRadixAttempt = 3;
   const int first_attempt = c->sort_start;
-  for (int attempt = first_attempt; attempt < 4; ++attempt) {
+  for (int attempt = first_attempt; attempt <= kRadixAttempt + 1; ++attempt) {
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {
@@ -699,6 +703,14 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortT0, hdr);
       TPX_LAUNCHED(c);
     } else if (attempt == 1) {
+      r.sort_T = kSortTm;
+      const uint32_t sort_tiles = n_tiles_of(n, kSortTm);
+      k_window_sort<20, kSortTm><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
+                                                                                            c->height, S, hdr);
+      TPX_LAUNCHED(c);
+      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortTm, hdr);
+      TPX_LAUNCHED(c);
+    } else if (attempt == 2) {
       r.sort_T = kSortT1;
       const uint32_t sort_tiles = n_tiles_of(n, kSortT1);
       k_window_sort<20, kSortT1><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
@@ -709,7 +721,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     } else {
       if ((rc = sort_global(c, r))) return rc;
     }
-    c->stats.sort_path = attempt >= 2 ? 1 : 0;
+    c->stats.sort_path = attempt >= kRadixAttempt ? 1 : 0;
     // one small read-back after the sort: validation and window-sort status
     // (a window wider than 32 bits of ticks leaves its output tile unwritten,
     // so the tile kernel must not run on it) and the window-density probe
@@ -727,7 +739,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       if ((rc = read_header(c, r))) return rc;  // synchronises the stream: the probe samples are in as well
       if (probe_on) memcpy(hprobe, c->host_scratch, sizeof(hprobe));
       if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
-      if (attempt < 2 && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
+      if (attempt < kRadixAttempt && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
         c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
         continue;
       }
@@ -741,23 +753,24 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       r.column = c->tile_mode == TPX_TILE_COLUMN;
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
-    c->stats.sort_retries = (attempt < 2 ? attempt : 2) - (first_attempt < 2 ? first_attempt : 2);
+    c->stats.sort_retries = (attempt < kRadixAttempt ? attempt : kRadixAttempt) -
+                            (first_attempt < kRadixAttempt ? first_attempt : kRadixAttempt);
     // the tile kernel indexes one bucket per pixel column (sparse) or packs
     // pixel ids in 20 bits (dense): larger sensors take the global pipeline
     const bool big_sensor =
         c->width > (uint32_t)kBuckets || (uint64_t)c->width * c->height + c->width > kMaxTilePixels;
-    c->bitmap_valid = !(attempt == 3 || big_sensor);
+    c->bitmap_valid = !(attempt == kRadixAttempt + 1 || big_sensor);
     rc = c->bitmap_valid ? cluster_sorted(c, r) : cluster_global(c, r);
     if (rc) return rc;
     if ((rc = read_header(c, r))) return rc;
     const dev_hdr& h = *c->host_hdr;
     if (h.err & 1u) return TPX_ERR_COORD_RANGE;
-    if (attempt < 2 && h.sort_bad) {  // displacement bound violated: widen / fall back
+    if (attempt < kRadixAttempt && h.sort_bad) {  // displacement bound violated: widen / fall back
       c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
       continue;
     }
-    if (attempt < 3 && (h.err & 2u)) {        // tile path inconsistency: global pipeline
-      attempt = 2;
+    if (attempt <= kRadixAttempt && (h.err & 2u)) {  // tile path inconsistency: global pipeline
+      attempt = kRadixAttempt;
       continue;
     }
     break;
