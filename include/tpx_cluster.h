@@ -127,10 +127,12 @@ int tpx_cluster_workspace_bytes(const tpx_cluster* ctx, uint64_t n,
  *   workspace    DEVICE, >= tpx_cluster_workspace_bytes(n), 256-B aligned.
  *   stream       cudaStream_t (NULL = legacy default stream).
  * All work is stream-ordered on `stream`; the call returns after the cluster
- * count has been read back (one small device->host copy + stream sync; a
- * second one after the sort carries its verification and the window-density
- * probe).  The windowed sort is verified before any clustering work; when its
- * displacement bound fails the run retries with a wider window, then the global
+ * count has been read back (a one-block kernel stores it into mapped pinned
+ * memory, then a stream sync -- no copy-engine transfer, so a run never waits
+ * behind another buffer's bulk copy; a second read-back after the sort carries
+ * its verification and the window-density probe).  The windowed sort is
+ * verified before any clustering work; when its displacement bound fails the
+ * run retries with wider windows (D = 1024, 2560, 3072), then the global
  * radix sort, and the context starts later runs at the attempt that succeeded
  * (results are identical on every path; tpx_run_stats reports the path).
  * n = 0 returns TPX_OK with 0 clusters.  The caller owns every buffer.
