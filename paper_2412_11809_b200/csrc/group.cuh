@@ -63,8 +63,23 @@ __global__ void k_group_first(const srec* __restrict__ S, uint64_t n, const uint
 __global__ void k_group_cpos(const srec* __restrict__ S, uint64_t n, const uint32_t* __restrict__ labels,
                              const uint32_t* __restrict__ rbits, const uint32_t* __restrict__ rbase,
                              uint32_t* __restrict__ cpos) {
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
-    cpos[p] = bit_rank(rbits, rbase, labels[__ldg(&S[p].idx)]);
+  // 4 positions per thread and iteration: their dependent load chains
+  // (index -> label -> rank words) are in flight together
+  constexpr int U = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += U * stride) {
+    uint32_t lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t p = p0 + u * stride;
+      lab[u] = p < n ? labels[__ldg(&S[p].idx)] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t p = p0 + u * stride;
+      if (p < n) cpos[p] = bit_rank(rbits, rbase, lab[u]);
+    }
+  }
 }
 
 // ... and the first position per cluster from its label.
