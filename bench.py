@@ -182,6 +182,34 @@ def _e2e(tpx, dt, n, h_host, lab_host, feat_host, cap_host, depth, e2e_steps):
     return e2e_ms, ks[-1]
 
 
+def _pcie_floor(n, h_host, lab_host, feat_host, k, steps):
+    import torch
+
+    d_in = [torch.empty(n * 16, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    d_lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    d_ft = torch.empty((max(k, 1), 64), dtype=torch.uint8, device="cuda")
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s_in)
+    s_out.wait_event(e0)
+    for i in range(steps):
+        with torch.cuda.stream(s_in):
+            d_in[i % 2].copy_(h_host, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+        s_out.wait_event(ev)
+        with torch.cuda.stream(s_out):
+            lab_host.copy_(d_lab, non_blocking=True)
+            feat_host[:k].copy_(d_ft[:k], non_blocking=True)
+    e1.record(s_out)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del d_in, d_lab, d_ft
+    torch.cuda.empty_cache()
+    return ms
+
+
 def _stream_e2e(tpx, dt, n, h_host, b):
     import torch
 
@@ -326,6 +354,12 @@ def run_ours(args):
     e2e_ms, kk = float("nan"), k
     if depth:
         e2e_ms, kk = _e2e(tpx, dt, n, h_host, lab_host, feat_host, cap_host, depth, e2e_steps)
+    # the same step's transfers alone on this box (H2D of the hits on one copy
+    # stream, D2H of labels + records on another, pipelined across steps):
+    # the PCIe floor the e2e number is bounded by (boxes differ)
+    pcie_floor_ms = None
+    if depth:
+        pcie_floor_ms = _pcie_floor(n, h_host, lab_host[0], feat_host[0], min(kk, cap_host), e2e_steps)
     del lab_host, feat_host
     # ---- exact streaming, host to host (tpx_stream_run_host: BufFill + carry
     # of border clusters, the paper's benchmark clock P:278-280), wall clock
@@ -387,7 +421,9 @@ def run_ours(args):
         "e2e": {"value": round(n / (e2e_ms * 1e-3) / 1e6, 2), "unit": "Mhit/s", "h2d_bytes_per_step": n * 16,
                 "d2h_bytes_per_step": n * 4 + min(kk, cap_host) * 64, "ms_per_step": round(e2e_ms, 3),
                 "api": f"tpx_pipeline_submit/wait (depth {depth}: copies of one buffer overlap the kernels of the others)",
-                "steps": e2e_steps},
+                "steps": e2e_steps,
+                "pcie_floor_ms_per_step": round(pcie_floor_ms, 3) if pcie_floor_ms else None,
+                "frac_of_pcie_floor": round(pcie_floor_ms / e2e_ms, 3) if pcie_floor_ms else None},
         "e2e_stream": stream_e2e,
         "grouped": grouped,
         "variants": variants,
