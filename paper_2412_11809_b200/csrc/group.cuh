@@ -160,7 +160,18 @@ __global__ void k_shapes_small(const tpx_hit* __restrict__ hits, const uint32_t*
     if (o1 - o0 >= kShapeWarpMin) continue;
     shape_acc s;
     s.init();
-    for (uint32_t j = o0; j < o1; ++j) {
+    uint32_t j = o0;
+    for (; j + 4 <= o1; j += 4) {  // 4 gathers in flight
+      uint32_t ix[4];
+      hit4 h[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ix[u] = order[j + u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) h[u] = load_hit(hits + ix[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s.add(h[u].x, h[u].y);
+    }
+    for (; j < o1; ++j) {
       const hit4 h = load_hit(hits + order[j]);
       s.add(h.x, h.y);
     }
