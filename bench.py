@@ -108,15 +108,44 @@ def _dist():
     return ws, rank, local
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class _PinnedCore:
+    """Pin the calling thread to one host core (sched_setaffinity) while the
+    single-threaded oracle is timed; restores the previous mask."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = max(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
+
+
 def cpu_baseline(h_sample, dt, label: str):
+    """The oracle as it stands, single-threaded, pinned to one core; returns
+    the timing record and the oracle's output (for the parity gate)."""
     import oracle
 
-    t0 = time.perf_counter()
-    oracle.cluster(h_sample, dt)
-    t = time.perf_counter() - t0
-    return {"value": len(h_sample) / t / 1e6, "unit": "Mhit/s", "cores": 1, "kind": "oracle",
-            "sample": label, "seconds": round(t, 3),
-            "host_cpus": os.cpu_count()}
+    with _PinnedCore() as pc:
+        t0 = time.perf_counter()
+        ref = oracle.cluster(h_sample, dt)
+        t = time.perf_counter() - t0
+    rec = {"value": len(h_sample) / t / 1e6, "unit": "Mhit/s", "cores": 1, "kind": "oracle",
+           "sample": label, "seconds": round(t, 3), "pinned_core": pc.core,
+           "host_cpus": os.cpu_count(), "cpu_model": _cpu_model()}
+    return rec, ref
 
 
 def run_reference(args):
@@ -134,10 +163,11 @@ def run_reference(args):
     for _ in range(args.warmup if args.warmup < 1 else 1):
         oracle.cluster(h[: min(len(h), 200_000)], p["dt_max"])
     times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.cluster(h, p["dt_max"])
-        times.append(time.perf_counter() - t0)
+    with _PinnedCore() as pc:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            oracle.cluster(h, p["dt_max"])
+            times.append(time.perf_counter() - t0)
     t = max(times) if times else float("nan")
     val = n_sample / (sum(times) / len(times)) / 1e6
     sample = f"first {n_sample} hits of {PRESET} (configs[2]) per step, single-threaded C oracle"
@@ -152,7 +182,8 @@ def run_reference(args):
         "config": {"workload": f"{PRESET} = BASELINE.json configs[2]: {n_work} hits, 40 Mhit/s shape, 80% gamma "
                                f"dots + 20% MIP tracks, dt_max=500 ns", "n_hits": n_work,
                    "dt_max_ticks": p["dt_max"], "sensor": "256x256", "sample_hits_per_step": n_sample},
-        "cpu_baseline": {"value": val, "unit": "Mhit/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "Mhit/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "pinned_core": pc.core, "host_cpus": os.cpu_count(), "cpu_model": _cpu_model()},
         "e2e": {"value": val, "unit": "Mhit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "max_step_s": t,
     }
@@ -238,6 +269,16 @@ def _stream_e2e(tpx, dt, n, h_host, b):
     return out
 
 
+def _full_invariants(tpx, labels, feats, n, k) -> bool:
+    gl = labels[:n].cpu().numpy().view(np.uint32)
+    gf = tpx.features_to_numpy(feats[:k])
+    ar = np.arange(n, dtype=np.uint32)
+    roots = np.flatnonzero(gl == ar)
+    ok = bool((gl <= ar).all() and np.array_equal(gl[gl], gl) and len(roots) == k
+              and np.array_equal(gf["label"].astype(np.int64), roots) and int(gf["size"].astype(np.int64).sum()) == n)
+    return ok
+
+
 def run_ours(args):
     import torch
 
@@ -287,6 +328,10 @@ def run_ours(args):
         torch.cuda.synchronize()
     c.set_profiling(False)
     ms = ev0.elapsed_time(ev1) / args.steps
+    # ---- properties of the timed run's output that hold at any size (no
+    # oracle): canonical labels (label[i] <= i, label[label[i]] == label[i]),
+    # one record per root in ascending label order, sizes summing to n
+    full_inv = _full_invariants(tpx, labels, feats, n, k)
     # ---- Step-6 grouped output + shape records (tpx_cluster_run_grouped, f3),
     # same input, device-timed
     grouped = None
@@ -403,11 +448,23 @@ def run_ours(args):
     whole_path_gbs = b_alg_hit * n / (ms * 1e-3) / 1e9
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
+    # and the parity gate: the GPU path on the same prefix through the same
+    # context, memcmp of labels and 64-B records against the oracle's output
     cpu = None
+    parity = {"status": "not checked", "full_invariants": full_inv}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         ns = min(args.ref_sample, n)
         sample = h_host[: ns * 16].numpy().view(tpxgen.HIT_DTYPE)
-        cpu = cpu_baseline(sample, dt, f"first {ns} hits of the same {PRESET} stream, single-threaded C oracle")
+        cpu, (rl, rf) = cpu_baseline(sample, dt, f"first {ns} hits of the same {PRESET} stream, single-threaded C oracle")
+        d_s = h_host[: ns * 16].to(dev)
+        sl, sf, sk = c.run(d_s, n=ns)
+        same_l = bool(np.array_equal(sl.cpu().numpy().view(np.uint32), rl))
+        same_f = bool(sk == len(rf) and tpx.features_to_numpy(sf).tobytes() == rf.tobytes())
+        del d_s, sl, sf
+        ok = same_l and same_f and full_inv
+        parity = {"status": "bit-exact" if ok else "MISMATCH", "prefix_hits": ns,
+                  "prefix_labels_memcmp": same_l, "prefix_records_memcmp": same_f, "full_invariants": full_inv,
+                  "full_size_memcmp": "tests/test_gpu_fullsize.py (configs[2] 200M, configs[3] 50M, configs[4] 250M shard)"}
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "Mhit/s", "n_gpus": ws, "steps": args.steps,
@@ -433,6 +490,7 @@ def run_ours(args):
         "hbm_frac_whole_path": round(whole_path_gbs / peak, 4),
         "stage_ms": {k_: round(v, 4) for k_, v in stage_avg.items()},
         "cpu_baseline": cpu,
+        "parity": parity,
         "clocks": clocks,
         "gen_seconds": round(gen_s, 2),
     }

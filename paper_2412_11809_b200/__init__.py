@@ -190,6 +190,9 @@ class Clusterer:
 
     def _workspace(self, nbytes: int, device):
         torch = _torch()
+        device = torch.device(device)
+        if device.type == "cuda" and device.index is None:  # "cuda" -> "cuda:<current>" (cache key)
+            device = torch.device("cuda", torch.cuda.current_device())
         if self._ws is None or self._ws.numel() < nbytes or self._ws.device != device:
             self._ws = None
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)

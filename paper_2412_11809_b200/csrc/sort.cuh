@@ -11,7 +11,8 @@ namespace tpx {
 struct dev_hdr {
   unsigned long long toa_min;
   unsigned long long toa_max;
-  unsigned int err;          // bit 0: coordinate / ToA range violation; bit 1: internal
+  unsigned int err;          // bit 0: coordinate / ToA range violation; bit 1: internal;
+                             // bit 2: a sort window spans >= 2^32 ticks (windowed sort impossible)
   unsigned int sort_bad;     // windowed-sort verification failures
   unsigned long long n_clusters;
   unsigned long long n_pairs;       // cross-tile union pairs

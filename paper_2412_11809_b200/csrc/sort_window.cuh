@@ -9,7 +9,8 @@
 // toa - window_min (ties keep input order => (toa, index) order), and writes
 // the middle T records.  Whether D held is verified afterwards: the
 // concatenation is correct iff it is strictly increasing in (toa, index)
-// across CTA borders (k_tile_cc checks every border); otherwise the host
+// across CTA borders (k_sort_check, run right after the sort, checks every
+// border and is the sole verifier); otherwise the host
 // retries with a larger D and finally with the global radix sort (sort.cuh).
 // Fused: coordinate / ToA-range validation of every hit.
 #pragma once
@@ -113,7 +114,10 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
   const unsigned long long top = block_max_u64(mx, red);
   const unsigned long long range = top - base;
   if (range >> 32) {  // window wider than 32 bits of ticks: leave it to the fallback
-    if (threadIdx.x == 0) atomicAdd(&hdr->sort_bad, 1u);
+    if (threadIdx.x == 0) {
+      atomicAdd(&hdr->sort_bad, 1u);
+      atomicOr(&hdr->err, 4u);  // a wider displacement bound cannot help: radix for this run only
+    }
     return;
   }
   const int bits = range ? 64 - __clzll(range) : 0;

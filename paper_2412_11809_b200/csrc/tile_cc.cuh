@@ -115,11 +115,22 @@ __device__ __forceinline__ bool adjacent(uint32_t a, uint32_t b) {
   return ((d & 0xffffu) <= 2u) & ((d >> 16) <= 2u);
 }
 
-__device__ __forceinline__ uint32_t s_find(volatile uint32_t* par, uint32_t x) {
+// Shared-memory atomic min without a return value (RED.MIN on shared memory).
+__device__ __forceinline__ void red_min_shared(uint32_t* p, uint32_t v) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+// Find with path halving.  Parents only decrease along a path (a root is
+// linked under a smaller one), so every ancestor is a valid parent and the
+// halving store can be an atomic min: concurrent finds on the same path then
+// never race (compute-sanitizer racecheck reports 0 hazards), and a halving
+// store can never move a node back down below a concurrently written one.
+__device__ __forceinline__ uint32_t s_find(uint32_t* par, uint32_t x) {
+  volatile uint32_t* vp = par;
   uint32_t p;
-  while ((p = par[x]) != x) {
-    const uint32_t g = par[p];
-    par[x] = g;
+  while ((p = vp[x]) != x) {
+    const uint32_t g = vp[p];
+    if (g != p) red_min_shared(par + x, g);
     x = g;
   }
   return x;
@@ -428,11 +439,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       s_meta[6] = srec_key_toa(S, f1 - 1);           // largest staged ToA
       s_meta[7] = ftrunc ? 2u : 0u;
     }
-  } else if (threadIdx.x == 64 && t0 > 0 && (t0 % a.verify_stride) == 0) {
-    // sort verification at sorted-tile borders: strictly increasing (toa, index)
-    const srec p = load_srec(S + t0 - 1), q = load_srec(S + t0);
-    const uint64_t tp = srec_toa(p), tq = srec_toa(q);
-    if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&a.hdr->sort_bad, 1u);
   }
   if constexpr (C::kHash) {
     for (uint32_t b = threadIdx.x; b < (uint32_t)C::kSlots; b += kTileThreads) tab[b] = 0xffffffffu;
@@ -797,9 +803,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
 
   // ---- flatten (read-only root walk; every stored value is a final root)
   for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
-    uint32_t c = par[l], nx;
+    const uint32_t p0 = par[l];
+    uint32_t c = p0, nx;
     while (c != (nx = par[c])) c = nx;
-    par[l] = c;
+    if (c != p0) red_min_shared(par + l, c);  // atomic: other threads' walks read par[l]
   }
   __syncthreads();
   TPX_PHASE(4);

@@ -159,7 +159,7 @@ __device__ __forceinline__ void tile_run_wide(const tile_args& a, uint64_t t0, u
 //   [3] back-truncated flag   [4] ToA of the first unstaged hit (if truncated)
 //   [5] ToA of the previous tile's last hit   [6] largest staged ToA
 //   [7] forward-truncated flag (2)
-// and the sort-order check at sorted-tile borders.
+// (the sort order itself is verified by k_sort_check right after the sort).
 template <class C>
 __global__ void __launch_bounds__(256) k_tile_bounds(const srec* __restrict__ S, uint64_t n, uint64_t dt,
                                                      uint32_t n_tiles, uint32_t verify_stride,
@@ -185,13 +185,6 @@ __global__ void __launch_bounds__(256) k_tile_bounds(const srec* __restrict__ S,
     case 5: v = t0 ? srec_key_toa(S, t0 - 1) : 0; break;
     case 6: v = srec_key_toa(S, f1 - 1); break;
     case 7: v = (ftrunc && srec_key_toa(S, flim) <= toa_last + dt) ? 2u : 0u; break;
-    case 8:
-      if (t0 > 0 && (t0 % verify_stride) == 0) {  // strictly increasing (toa, index)
-        const srec p = load_srec(S + t0 - 1), q = load_srec(S + t0);
-        const uint64_t tp = srec_toa(p), tq = srec_toa(q);
-        if (!(tp < tq || (tp == tq && p.idx < q.idx))) atomicAdd(&hdr->sort_bad, 1u);
-      }
-      break;
     default: break;
   }
   if (lane < 8) meta[(uint64_t)t * 8 + lane] = v;
@@ -448,15 +441,27 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
   TPX_PHASE(3);
 
   // ---- flatten; multi-hit marks; open marks; cross pairs (halo hits that
-  // joined a tile component)
-  for (uint32_t h0 = 0; h0 < m; h0 += kTh) {
-    const uint32_t l = h0 + threadIdx.x;
-    bool joined = false;
+  // joined a tile component).  Roots are found first (reads only), stored
+  // after a barrier: no thread writes a parent another thread's walk reads.
+  uint32_t root[C::kStage];
+#pragma unroll
+  for (int s = 0; s < C::kStage; ++s) {
+    const uint32_t l = threadIdx.x + s * kTh;
     uint32_t c = 0;
     if (l < m) {
       uint32_t nx;
       c = par[l];
       while (c != (nx = par[c])) c = nx;
+    }
+    root[s] = c;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < C::kStage; ++s) {
+    const uint32_t l = threadIdx.x + s * kTh;
+    const uint32_t c = root[s];
+    bool joined = false;
+    if (l < m) {
       par[l] = c;
       if (l < nt) {
         if (c != l) multi[c] = 1;

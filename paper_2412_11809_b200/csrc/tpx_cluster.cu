@@ -105,7 +105,11 @@ struct tpx_cluster {
   int want_first;    // next run records each cluster's first sorted position (grouped runs)
   int sort_start;  // first sort attempt (0: D=1024 window, 1: D=2560, 2: D=3072, 3: global radix);
                    // raised to the attempt that succeeded, so a stream whose disorder exceeds
-                   // the window bound pays the failed attempts once, not on every run
+                   // the window bound pays the failed attempts once, not on every run; it
+                   // decays back to 0 after kSortProbeRuns runs (the stream may have calmed
+                   // down), and a window spanning >= 2^32 ticks (a beam pause) sends only
+                   // that run to the radix sort without raising it
+  int runs_at_start;  // runs since sort_start was last raised
   tpx_cluster* island;  // variants (b)/(c): (a)-context whose components are the islands
   uint64_t island_dt;
 };
@@ -690,6 +694,11 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   // attempt 3: global radix sort; attempt 4: global union-find pipeline
   // (internal fallback)
   constexpr int kRadixAttempt = 3;
+  constexpr int kSortProbeRuns = 64;
+  if (c->sort_start > 0 && ++c->runs_at_start > kSortProbeRuns) {
+    c->sort_start = 0;
+    c->runs_at_start = 0;
+  }
   const int first_attempt = c->sort_start;
   for (int attempt = first_attempt; attempt <= kRadixAttempt + 1; ++attempt) {
     if ((rc = reset_header(c, r))) return rc;
@@ -739,8 +748,15 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       if ((rc = read_header(c, r))) return rc;  // synchronises the stream: the probe samples are in as well
       if (probe_on) memcpy(hprobe, c->host_scratch, sizeof(hprobe));
       if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
+      if (attempt < kRadixAttempt && (c->host_hdr->err & 4u)) {  // >= 2^32-tick window: radix, this run only
+        attempt = kRadixAttempt - 1;
+        continue;
+      }
       if (attempt < kRadixAttempt && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
-        c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
+        if (attempt + 1 > c->sort_start) {
+          c->sort_start = attempt + 1;
+          c->runs_at_start = 0;
+        }
         continue;
       }
       if (probe_on) {
@@ -766,7 +782,10 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     const dev_hdr& h = *c->host_hdr;
     if (h.err & 1u) return TPX_ERR_COORD_RANGE;
     if (attempt < kRadixAttempt && h.sort_bad) {  // displacement bound violated: widen / fall back
-      c->sort_start = attempt + 1 > c->sort_start ? attempt + 1 : c->sort_start;
+      if (attempt + 1 > c->sort_start) {
+        c->sort_start = attempt + 1;
+        c->runs_at_start = 0;
+      }
       continue;
     }
     if (attempt <= kRadixAttempt && (h.err & 2u)) {  // tile path inconsistency: global pipeline

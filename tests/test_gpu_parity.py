@@ -286,36 +286,7 @@ def test_run_host_matches_device(tpx):
     assert tpx.features_to_numpy(feats[:k]).tobytes() == rf.tobytes()
 
 
-# ------------------------------------------- full BASELINE size, sampled parity
-@pytest.mark.slow
-@pytest.mark.parametrize("preset,n", [("mixed", None), ("heavyion", None), ("timepix4", 250_000_000)])
-def test_full_size_sampled(tpx, preset, n):
-    """configs[2] (200M) / configs[3] (50M) in the launch configuration
-    bench.py times, and configs[4]'s per-GPU shard (2B hits / 8 GPUs = 250M
-    on the 448x512 sensor); oracle components computed one by one for a
-    sample of hits, plus properties that hold at any size."""
-    p = tpxgen.PRESETS[preset]
-    h = tpxgen.generate(preset, n_hits=n)
-    n = len(h)
-    W, H = (448, 512) if preset == "timepix4" else (256, 256)
-    gl, gf, k, gc, st = _gpu(tpx, h, p["dt_max"], W, H)
-    # properties: canonical labels, partition sums, ordering
-    assert (gl <= np.arange(n, dtype=np.uint32)).all()
-    assert np.array_equal(gl[gl], gl)
-    assert int(gf["size"].astype(np.uint64).sum()) == n
-    assert int(gf["tot_sum"].sum()) == int(h["tot"].astype(np.uint64).sum())
-    assert (np.diff(gf["label"].astype(np.int64)) > 0).all()
-    assert k == int((gl == np.arange(n, dtype=np.uint32)).sum())
-    # sampled oracle components
-    s = oracle.ComponentSampler(h, p["dt_max"], W, H)
-    rng = np.random.default_rng(17)
-    for seed in rng.integers(0, n, 400).tolist():
-        f = s.component(seed)
-        assert gl[seed] == f["label"]
-        row = gf[np.searchsorted(gf["label"], f["label"])]
-        for name in pins.FEAT_FIELDS:
-            assert int(row[name]) == int(f[name]), (seed, name)
-    s.close()
+# Full BASELINE sizes: element-by-element parity in tests/test_gpu_fullsize.py.
 
 
 def test_pipeline_matches_run_host(tpx):
