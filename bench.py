@@ -499,11 +499,6 @@ def run_ours(args):
     return 0
 
 
-# kernels launched per call of each sharded building block (see tpx_cluster.cu)
-_SHARD_LAUNCHES = {"toa_range": 2, "select_halo": 5, "translate": 1, "offset": 1, "gather": 1, "pairs": 1,
-                   "union": 27, "relabel": 1, "split": 5, "fold": 27}
-
-
 def run_ours_multi(args):
     """N GPUs of one node, one process per GPU (torchrun), NCCL over NVLink.
     Strong scaling: the fixed configs[2] stream (200M hits) is split into N
@@ -512,8 +507,9 @@ def run_ours_multi(args):
     import torch.distributed as dist
 
     ws, rank, local = _dist()
-    # NCCL over NVLink, one GPU per rank.  TPX_DIST_BACKEND=gloo is a
-    # functional mode (ranks may share a GPU; collectives staged via the host).
+    # NCCL over NVLink, one GPU per rank (library-owned communicator,
+    # tpx_nccl_comm_init).  TPX_DIST_BACKEND=gloo is a functional mode (ranks
+    # may share a GPU; the library's host-callback transport).
     backend = os.environ.get("TPX_DIST_BACKEND", "nccl")
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
@@ -550,12 +546,14 @@ def run_ours_multi(args):
         os.remove(path)
     gen_s = time.time() - t0
     d_hits = h_host.to(dev)
-    comm = sharded.TorchComm(staged=(backend != "nccl"))
-    ops = sharded.CudaOps(dt)
+    comm = sharded.NcclComm() if backend == "nccl" else sharded.HostComm(sharded.TorchAdapter())
+    sc = sharded.ShardedClusterer(dt, comm)
     stream = torch.cuda.current_stream(dev)
+    lab_d = torch.empty(nr, dtype=torch.int32, device=dev)
+    ft_d = torch.empty((nr, 64), dtype=torch.uint8, device=dev)
 
     def step(x):
-        return sharded.cluster_sharded(x, dt, comm, ops)
+        return sc.run(x, labels=lab_d, features=ft_d, stream=stream)
 
     for _ in range(args.warmup):
         res = step(d_hits)
@@ -580,7 +578,7 @@ def run_ours_multi(args):
     st = res.stats
     k_total = torch.tensor([res.n_clusters], device=rdev, dtype=torch.int64)
     dist.all_reduce(k_total)
-    launches_step = ops.clusterer.stats()["kernel_launches"] + sum(_SHARD_LAUNCHES.values())
+    launches_step = st["kernel_launches"]
 
     # ---- end to end: pinned host block -> HBM, sharded run, labels + records -> host
     lab_host = torch.empty(nr, dtype=torch.int32).pin_memory()
@@ -602,7 +600,8 @@ def run_ours_multi(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     gathered = [None] * ws
-    dist.all_gather_object(gathered, {"rank": rank, "n": nr, "ms": ms_local, **st})
+    dist.all_gather_object(gathered, {"rank": rank, "n": nr, "ms": ms_local,
+                                      **{k_: v for k_, v in st.items() if k_ != "tile_phase_cycles"}})
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "Mhit/s", "n_gpus": ws, "steps": args.steps,

@@ -311,96 +311,101 @@ int tpx_pipeline_elapsed_ms(tpx_pipeline* p, float* ms);
 void tpx_pipeline_destroy(tpx_pipeline* p);
 
 /* ------------------------------------------------------------------------
- * ToA-sharded multi-GPU building blocks (one process per GPU).
+ * ToA-sharded multi-GPU clustering; one process per
+ * GPU, one rank per process.
  *
- * Rank r owns the contiguous input-index block [o_r, o_r + n_r) of the
- * t-ordered stream (§3.1 l.99-100).  Edges only join hits within
- * dt_max in ToA (§2 (iii)(a) l.39), so rank r needs only rank r+1's hits with
- * toa <= maxToA(r) + dt_max (the temporal-splitting border region, §3.2.3
- * l.117-119), provided no edge can skip a rank (minToA(r+2) > maxToA(r) +
- * dt_max, checked by the caller from the gathered ranges).  The collectives
- * between these calls (all-gather of sizes/ranges/pairs/partials, halo
- * send/recv) are issued by the caller on its process group (NCCL over
- * NVLink); every compute step below is a device kernel.  All pointers are
- * DEVICE pointers, all calls are stream-ordered and asynchronous unless
- * stated, `count`-style outputs are device uint64 written by the call.
+ * Method: temporal splitting (§3.2.3 l.117-119: "we only need to
+ * examine the dt_max-time neighborhood around each border") with the GPU's
+ * border stitching (§4 l.173).  Rank r owns the contiguous input-index block
+ * [o_r, o_r + n_r) of the t-ordered stream (§3.1 l.99-100), o_r = n_0 + ... +
+ * n_{r-1}.  Edges only join hits within dt_max in ToA (§2 (iii)(a) l.39), so
+ * every edge between ranks r and r+1 has its rank-(r+1) end among the hits
+ * with toa <= maxToA(r) + dt_max (the "halo" rank r+1 lends to rank r),
+ * provided no edge skips a rank: minToA(r+2) > maxToA(r) + dt_max for every r
+ * (checked; TPX_ERR_UNSUPPORTED otherwise).  One run:
+ *   1. all-gather [n_r, minToA, maxToA] (+ halo counts); rank r+1 selects and
+ *      sends its halo to rank r (NCCL send/recv);
+ *   2. each rank clusters [owned | halo] (the tpx_cluster_run kernels; only
+ *      owned hits contribute features), labels written as global indices;
+ *   3. rank r+1 returns its labels of the lent hits; each (label on r, label
+ *      on r+1) pair of a halo hit is all-gathered, every rank unites all
+ *      pairs (smallest label wins = label of the merged cluster, reading R6);
+ *   4. owned labels are relabelled; records of clusters whose final label is
+ *      elsewhere are all-gathered as partials and folded (integer add / min /
+ *      max: exact, order independent) by the rank owning the final label.
+ * Output: labels of the owned hits (global input indices) and the records of
+ * the clusters whose label falls in [o_r, o_r + n_r), ascending -- so the
+ * ranks' outputs concatenated in rank order equal tpx_cluster_run on the
+ * whole stream byte for byte.  Variant (iii)(a) only.
  * ---------------------------------------------------------------------- */
 
-/* minmax[0] = min toa, minmax[1] = max toa of n hits (n = 0: ~0, 0). */
-int tpx_shard_toa_range(const tpx_hit* hits, uint64_t n, uint64_t* minmax,
-                        void* stream);
+typedef struct tpx_comm tpx_comm;
 
-int tpx_shard_select_workspace_bytes(uint64_t n, size_t* bytes);
+/* NCCL bootstrap (multi-GPU product path).  Rank 0 calls tpx_nccl_unique_id
+ * and distributes the 128 bytes to every rank (e.g. over the torch process
+ * group); every rank then calls tpx_nccl_comm_init on its own CUDA device
+ * (the current device of the calling thread).  The communicator is owned by
+ * the library (tpx_comm_destroy frees it).  libnccl.so.2 is loaded with
+ * dlopen on first use.  Errors: NCCL (library missing or an NCCL call
+ * failed), INVALID_ARG. */
+int tpx_nccl_unique_id(uint8_t id_out[128]);
+int tpx_nccl_comm_init(int rank, int world, const uint8_t id[128],
+                       tpx_comm** out);
 
-/* Halo for the previous rank: the hits with toa <= toa_limit, compacted in
- * input order into halo_out, their positions (0-based, this rank's block)
- * into idx_out; *count = how many.  Capacity of halo_out / idx_out: n. */
-int tpx_shard_select_halo(const tpx_hit* hits, uint64_t n, uint64_t toa_limit,
-                          tpx_hit* halo_out, uint32_t* idx_out,
-                          uint64_t* count, void* workspace,
-                          size_t workspace_bytes, void* stream);
+/* Host-callback transport (functional runs where NCCL cannot be used:
+ * in-process virtual ranks, gloo process groups, several ranks on one GPU).
+ * Device buffers are staged through pinned host memory.  Callbacks return 0
+ * on success; HOST pointers:
+ *   allgather(user, send, recv, bytes): recv[r*bytes .. (r+1)*bytes) =
+ *       rank r's send (bytes each, world ranks);
+ *   sendrecv(user, to, send, send_bytes, from, recv, recv_bytes): send to
+ *       rank `to` and receive from rank `from` (-1: none) concurrently. */
+typedef int (*tpx_allgather_fn)(void* user, const void* send, void* recv,
+                                size_t bytes);
+typedef int (*tpx_sendrecv_fn)(void* user, int to, const void* send,
+                               size_t send_bytes, int from, void* recv,
+                               size_t recv_bytes);
+int tpx_comm_create_host(int rank, int world, tpx_allgather_fn allgather,
+                         tpx_sendrecv_fn sendrecv, void* user, tpx_comm** out);
 
-/* Local labels of [owned (n_owned) | halo (n - n_owned)] -> global input
- * indices: L < n_owned -> own_offset + L, else next_offset + halo_idx[L - n_owned]. */
-int tpx_shard_translate_labels(uint32_t* labels, uint64_t n, uint64_t n_owned,
-                               uint64_t own_offset, const uint32_t* halo_idx,
-                               uint64_t next_offset, void* stream);
+void tpx_comm_destroy(tpx_comm* comm);
+int tpx_comm_rank(const tpx_comm* comm, int* rank, int* world);
 
-/* features[i].label += offset for i < k (local -> global labels). */
-int tpx_shard_offset_labels(tpx_cluster_features* features, uint64_t k,
-                            uint64_t offset, void* stream);
+/* Host-buffer self test of a communicator (no GPU needed for host
+ * transports): every rank all-gathers `bytes` bytes of a rank-dependent
+ * pattern and exchanges a pattern with its neighbours (to r-1, from r+1);
+ * returns TPX_OK iff every received byte is as expected. */
+int tpx_comm_selftest(tpx_comm* comm, size_t bytes);
 
-/* out[k] = labels[idx[k]], k < count (labels of the hits sent as halo). */
-int tpx_shard_gather_labels(const uint32_t* labels, const uint32_t* idx,
-                            uint64_t count, uint32_t* out, void* stream);
+/* Device workspace of tpx_cluster_run_sharded for n_local owned hits on a
+ * communicator of `world` ranks (bytes). */
+int tpx_cluster_sharded_workspace_bytes(const tpx_cluster* ctx, uint64_t n_local,
+                                        int world, size_t* bytes);
 
-/* Boundary pairs: (a[k], b[k]) for every k with a[k] != b[k], compacted into
- * pairs_out (2 u32 per pair, capacity 2*count); *n_pairs = how many. */
-int tpx_shard_make_pairs(const uint32_t* a, const uint32_t* b, uint64_t count,
-                         uint32_t* pairs_out, uint64_t* n_pairs, void* stream);
+/* Halo capacity: hits one rank may lend to the previous one per run
+ * (TPX_ERR_UNSUPPORTED beyond; ~ rate x (readout disorder + dt_max)). */
+#define TPX_SHARD_HALO_CAP (1u << 18)
 
-int tpx_shard_union_workspace_bytes(uint64_t n_pairs, size_t* bytes);
-
-/* Union pass over all ranks' pairs (n_pairs known on the host): map_keys =
- * the distinct labels appearing in pairs, ascending; map_vals = the smallest
- * label connected to each; *n_map = number of keys (capacity 2*n_pairs). */
-int tpx_shard_union_pairs(const uint32_t* pairs, uint64_t n_pairs,
-                          uint32_t* map_keys, uint32_t* map_vals,
-                          uint64_t* n_map, void* workspace,
-                          size_t workspace_bytes, void* stream);
-
-/* labels[i] <- map(labels[i]) for labels that are map keys. */
-int tpx_shard_relabel(uint32_t* labels, uint64_t n, const uint32_t* map_keys,
-                      const uint32_t* map_vals, const uint64_t* n_map,
-                      void* stream);
-
-int tpx_shard_split_workspace_bytes(uint64_t k, size_t* bytes);
-
-/* Split k label-sorted records: records whose label is a map key become
- * partials keyed by their final label (partials_out, *n_partials, any order);
- * the others are kept in order (kept_out, *n_kept).  Capacities: k each. */
-int tpx_shard_split_features(const tpx_cluster_features* features, uint64_t k,
-                             const uint32_t* map_keys, const uint32_t* map_vals,
-                             const uint64_t* n_map,
-                             tpx_cluster_features* kept_out, uint64_t* n_kept,
-                             tpx_cluster_features* partials_out,
-                             uint64_t* n_partials, void* workspace,
-                             size_t workspace_bytes, void* stream);
-
-int tpx_shard_fold_workspace_bytes(uint64_t n_partials, size_t* bytes);
-
-/* Owner fold: partials (all ranks') with label in [label_lo, label_hi) are
- * combined per label (integer add / min / max: order independent, exact) and
- * merged with the kept records into out (ascending label).  *n_out (HOST) =
- * record count; synchronises the stream.  TPX_ERR_CAPACITY if it exceeds
- * capacity. */
-int tpx_shard_fold_features(const tpx_cluster_features* kept, uint64_t n_kept,
-                            const tpx_cluster_features* partials,
-                            uint64_t n_partials, uint64_t label_lo,
-                            uint64_t label_hi, tpx_cluster_features* out,
-                            uint64_t capacity, uint64_t* n_out,
-                            void* workspace, size_t workspace_bytes,
-                            void* stream);
+/* The sharded run (every rank calls it, collectively, on its own stream).
+ *   local_hits        DEVICE, n_local >= 1 owned hits (the block), 16-B aligned
+ *   labels_out_local  DEVICE, n_local entries: global labels of owned hits
+ *   features_out_local DEVICE, capacity records: clusters whose label is in
+ *                     this rank's block, ascending label
+ *   n_local_clusters_out HOST: number of those records (> capacity: CAPACITY,
+ *                     labels valid, records truncated)
+ *   global_offset_out HOST, may be NULL: o_r
+ * Total hits < 2^32 - 1.  Host synchronisations: 3 (counts after the halo
+ * exchange, the sort status, the final count).  Errors: INVALID_ARG,
+ * UNSUPPORTED (variant, sensor wider than 1024 px, a rank-skipping edge, halo
+ * above TPX_SHARD_HALO_CAP), COORD_RANGE, TOO_MANY_HITS, CAPACITY, OOM, CUDA,
+ * NCCL -- the same status on every rank. */
+int tpx_cluster_run_sharded(tpx_cluster* ctx, tpx_comm* comm,
+                            const tpx_hit* local_hits, uint64_t n_local,
+                            uint32_t* labels_out_local,
+                            tpx_cluster_features* features_out_local,
+                            uint64_t capacity, uint64_t* n_local_clusters_out,
+                            uint64_t* global_offset_out, void* workspace,
+                            size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * Streaming ingest: Alg. "Hit buffer filling" (PAPER.md

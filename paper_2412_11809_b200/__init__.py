@@ -86,23 +86,19 @@ _pipe_wait = _proto("tpx_pipeline_wait", _int, _vp, _u64, ctypes.POINTER(_u64))
 _pipe_mark = _proto("tpx_pipeline_mark", _int, _vp, _int)
 _pipe_elapsed = _proto("tpx_pipeline_elapsed_ms", _int, _vp, ctypes.POINTER(ctypes.c_float))
 _pipe_destroy = _proto("tpx_pipeline_destroy", None, _vp)
-# sharded building blocks (include/tpx_cluster.h, "ToA-sharded multi-GPU")
-_shard_toa_range = _proto("tpx_shard_toa_range", _int, _vp, _u64, _vp, _vp)
-_shard_select_ws = _proto("tpx_shard_select_workspace_bytes", _int, _u64, _size_t_p)
-_shard_select = _proto("tpx_shard_select_halo", _int, _vp, _u64, _u64, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp)
-_shard_translate = _proto("tpx_shard_translate_labels", _int, _vp, _u64, _u64, _u64, _vp, _u64, _vp)
-_shard_gather = _proto("tpx_shard_gather_labels", _int, _vp, _vp, _u64, _vp, _vp)
-_shard_offset = _proto("tpx_shard_offset_labels", _int, _vp, _u64, _u64, _vp)
-_shard_pairs = _proto("tpx_shard_make_pairs", _int, _vp, _vp, _u64, _vp, _vp, _vp)
-_shard_union_ws = _proto("tpx_shard_union_workspace_bytes", _int, _u64, _size_t_p)
-_shard_union = _proto("tpx_shard_union_pairs", _int, _vp, _u64, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp)
-_shard_relabel = _proto("tpx_shard_relabel", _int, _vp, _u64, _vp, _vp, _vp, _vp)
-_shard_split_ws = _proto("tpx_shard_split_workspace_bytes", _int, _u64, _size_t_p)
-_shard_split = _proto("tpx_shard_split_features", _int, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                      ctypes.c_size_t, _vp)
-_shard_fold_ws = _proto("tpx_shard_fold_workspace_bytes", _int, _u64, _size_t_p)
-_shard_fold = _proto("tpx_shard_fold_features", _int, _vp, _u64, _vp, _u64, _u64, _u64, _vp, _u64,
-                     ctypes.POINTER(_u64), _vp, ctypes.c_size_t, _vp)
+# ToA-sharded run + communicators (include/tpx_cluster.h, "ToA-sharded multi-GPU clustering")
+ALLGATHER_FN = ctypes.CFUNCTYPE(_int, _vp, _vp, _vp, ctypes.c_size_t)
+SENDRECV_FN = ctypes.CFUNCTYPE(_int, _vp, _int, _vp, ctypes.c_size_t, _int, _vp, ctypes.c_size_t)
+_nccl_unique_id = _proto("tpx_nccl_unique_id", _int, ctypes.c_char_p)
+_nccl_comm_init = _proto("tpx_nccl_comm_init", _int, _int, _int, ctypes.c_char_p, ctypes.POINTER(_vp))
+_comm_create_host = _proto("tpx_comm_create_host", _int, _int, _int, ALLGATHER_FN, SENDRECV_FN, _vp,
+                           ctypes.POINTER(_vp))
+_comm_destroy = _proto("tpx_comm_destroy", None, _vp)
+_comm_rank = _proto("tpx_comm_rank", _int, _vp, ctypes.POINTER(_int), ctypes.POINTER(_int))
+_comm_selftest = _proto("tpx_comm_selftest", _int, _vp, ctypes.c_size_t)
+_sharded_ws = _proto("tpx_cluster_sharded_workspace_bytes", _int, _vp, _u64, _int, _size_t_p)
+_run_sharded = _proto("tpx_cluster_run_sharded", _int, _vp, _vp, _vp, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
+                      ctypes.POINTER(_u64), _vp, ctypes.c_size_t, _vp)
 
 ABI_VERSION = _abi_version()
 

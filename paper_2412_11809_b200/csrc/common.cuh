@@ -58,6 +58,19 @@ __device__ __forceinline__ hit4 load_hit(const tpx_hit* h) {
   return r;
 }
 
+// Input of the sort kernels: one array, or two concatenated segments (the
+// sharded path sorts [owned hits | halo received from the next rank] without
+// copying the caller's owned hits): element i is a[i] for i < na, else
+// b[i - na].  Implicit from a plain pointer (one segment).
+struct hit_src {
+  const tpx_hit* a;
+  const tpx_hit* b;
+  uint64_t na;
+  __host__ __device__ hit_src(const tpx_hit* p = nullptr) : a(p), b(nullptr), na(~0ull) {}
+  __host__ __device__ hit_src(const tpx_hit* p, uint64_t n1, const tpx_hit* q) : a(p), b(q), na(n1) {}
+  __device__ __forceinline__ const tpx_hit* operator+(uint64_t i) const { return i < na ? a + i : b + (i - na); }
+};
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

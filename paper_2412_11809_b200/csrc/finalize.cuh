@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
                                                               const uint32_t* __restrict__ slot_of,
                                                               const tpx_cluster_features* __restrict__ stage,
                                                               uint32_t* __restrict__ labels, uint32_t* bitmap,
-                                                              uint32_t n_owned, uint32_t* __restrict__ first_of_label) {
+                                                              uint32_t n_owned, uint32_t* __restrict__ first_of_label,
+                                                              label_map lm) {
   const uint64_t nh = hdr->n_open_hits, nc = hdr->n_open_comps;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   constexpr int U = 4;  // 4 dependent load chains in flight per thread
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (pos[u] != 0xffffffffu) labels[idx[u]] = lab[u];
+      if (pos[u] != 0xffffffffu) store_label(labels, n_owned, lm, idx[u], lab[u]);
   }
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += stride) {
     const uint32_t r = open_comps[t];
@@ -194,7 +195,9 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
                                                        uint32_t tile,
                                                        const uint32_t* __restrict__ bitmap,
                                                        const uint32_t* __restrict__ wbase,
-                                                       tpx_cluster_features* __restrict__ out, uint64_t capacity) {
+                                                       tpx_cluster_features* __restrict__ out, uint64_t capacity,
+                                                       uint32_t label_off, tpx_cluster_features* __restrict__ removed,
+                                                       unsigned long long* n_removed) {
   const unsigned lane = lane_id();
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
@@ -210,7 +213,19 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
       const uint32_t size = __shfl_sync(kFull, v.y, lane & ~3u);
       if (!valid || size == 0) continue;
       const uint32_t w = label >> 5;
-      const uint64_t ord = (uint64_t)wbase[w] + __popc(bitmap[w] & ((1u << (label & 31)) - 1u));
+      const uint32_t bits = bitmap[w];
+      if ((q & 3) == 0) v.x = label + label_off;  // global label (sharded runs)
+      if (!((bits >> (label & 31)) & 1u)) {
+        // bit cleared by the sharded boundary merge: the record moves to the
+        // rank owning the cluster's final label (one slot per record)
+        if (!removed) continue;
+        uint32_t slot = 0;
+        if ((q & 3) == 0) slot = (uint32_t)atomicAdd(n_removed, 1ull);
+        slot = __shfl_sync(0xfu << (lane & ~3u), slot, lane & ~3u);  // the record's 4 lanes take this branch together
+        reinterpret_cast<uint4*>(removed + slot)[q & 3] = v;
+        continue;
+      }
+      const uint64_t ord = (uint64_t)wbase[w] + __popc(bits & ((1u << (label & 31)) - 1u));
       if (ord >= capacity) continue;
       reinterpret_cast<uint4*>(out + ord)[q & 3] = v;
     }

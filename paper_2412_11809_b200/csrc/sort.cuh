@@ -27,7 +27,7 @@ static_assert(sizeof(dev_hdr) == 256, "dev_hdr layout");
 constexpr int kMMThreads = 256;
 
 // Fused validation + min/max ToA (one read of the hits).
-__global__ void __launch_bounds__(kMMThreads) k_validate_minmax(const tpx_hit* __restrict__ hits, uint64_t n,
+__global__ void __launch_bounds__(kMMThreads) k_validate_minmax(hit_src hits, uint64_t n,
                                                                 uint32_t width, uint32_t height,
                                                                 dev_hdr* hdr) {
   uint64_t mn = ~0ull, mx = 0;
@@ -64,7 +64,7 @@ constexpr int kRadixBins = 256;
 #endif
 
 template <typename KeyT, bool kFromHits>
-__device__ __forceinline__ KeyT radix_key(const tpx_hit* hits, const KeyT* keys, uint64_t i, uint64_t toa_min) {
+__device__ __forceinline__ KeyT radix_key(const hit_src& hits, const KeyT* keys, uint64_t i, uint64_t toa_min) {
   if constexpr (kFromHits) {
     return (KeyT)(load_hit(hits + i).toa - toa_min);
   } else {
@@ -74,7 +74,7 @@ __device__ __forceinline__ KeyT radix_key(const tpx_hit* hits, const KeyT* keys,
 
 // Per-tile digit histogram, written digit-major: hist[d * n_tiles + tile].
 template <typename KeyT, bool kFromHits>
-__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const tpx_hit* __restrict__ hits,
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(hit_src hits,
                                                              const KeyT* __restrict__ keys, uint64_t n,
                                                              uint64_t toa_min, int shift,
                                                              uint32_t* __restrict__ hist, uint32_t n_tiles) {
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const tpx_hit* __r
 // Stable scatter: rank = global digit offset of this tile + number of earlier
 // (round, warp, lane)-ordered elements of the tile with the same digit.
 template <typename KeyT, bool kFromHits>
-__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const tpx_hit* __restrict__ hits,
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(hit_src hits,
                                                                 const KeyT* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in, uint64_t n,
                                                                 uint64_t toa_min, int shift,
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const tpx_hit* 
 // stores coalesce, and the tile needs four barriers instead of three per
 // 256 elements.
 template <bool kFromHits>
-__global__ void __launch_bounds__(kRadixThreads, TPX_RSCAT_MINB) k_radix_scatter_tile(const tpx_hit* __restrict__ hits,
+__global__ void __launch_bounds__(kRadixThreads, TPX_RSCAT_MINB) k_radix_scatter_tile(hit_src hits,
                                                                      const uint32_t* __restrict__ keys_in,
                                                                      const uint32_t* __restrict__ vals_in,
                                                                      uint64_t n, uint64_t toa_min, int shift,
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_RSCAT_MINB) k_radix_scatter
 // Sorted records + union-find init: rec[i] = hit[perm[i]], parent[i] = i.
 // Four elements per thread and iteration: the permutation loads, then the
 // dependent hit gathers, are issued together (memory-level parallelism).
-__global__ void k_gather_init(const tpx_hit* __restrict__ hits, const uint32_t* __restrict__ perm, uint64_t n,
+__global__ void k_gather_init(hit_src hits, const uint32_t* __restrict__ perm, uint64_t n,
                               srec* __restrict__ rec, uint32_t* __restrict__ parent) {
   constexpr int U = 4;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

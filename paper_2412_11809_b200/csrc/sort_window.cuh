@@ -77,7 +77,7 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 }
 
 template <int IT, int T>
-__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit* __restrict__ hits, uint64_t n,
+__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, uint64_t n,
                                                                    uint32_t width, uint32_t height,
                                                                    srec* __restrict__ out, dev_hdr* hdr) {
   using C = wsort_cfg<IT, T>;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(const tpx_hit*
     const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
     toa[r] = 0;
     if (p < m) {
-      hit4 h = load_hit(hits + ws + p);
+      hit4 h = load_hit(hits + (ws + p));
       toa[r] = h.toa;
       mn = min(mn, (unsigned long long)h.toa);
       mx = max(mx, (unsigned long long)h.toa);

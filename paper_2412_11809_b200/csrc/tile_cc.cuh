@@ -73,6 +73,27 @@ struct tile_cfg {
 using tile_sparse = tile_cfg<1024, 256, 1024, 4, false>;
 using tile_dense = tile_cfg<4096, 1024, 4096, 1, true>;
 
+// Where the final label of a hit goes (sharded runs, sharded.cuh): labels of
+// owned hits (input index < n_owned) into `labels`, of halo hits into
+// `halo_labels`, translated to global input indices -- own_off + l for an
+// owned label l, next_off + halo_idx[l - n_owned] for a label that is a halo
+// hit.  halo_idx == nullptr: one array, local labels (every other run).
+struct label_map {
+  uint32_t* halo_labels;
+  const uint32_t* halo_idx;
+  uint32_t own_off, next_off;
+};
+__device__ __forceinline__ void store_label(uint32_t* labels, uint32_t n_owned, const label_map& m, uint32_t idx,
+                                            uint32_t label) {
+  if (!m.halo_idx) {
+    labels[idx] = label;
+    return;
+  }
+  const uint32_t g = label < n_owned ? label + m.own_off : m.next_off + m.halo_idx[label - n_owned];
+  if (idx < n_owned) labels[idx] = g;
+  else m.halo_labels[idx - n_owned] = g;
+}
+
 struct tile_args {
   const srec* S;
   uint64_t n;
@@ -95,6 +116,7 @@ struct tile_args {
   unsigned long long* phase_cycles;  // optional per-phase clock totals (profiling), may be null
   const uint64_t* tile_meta;  // k_tile_bounds output (k_tile_cell only)
   uint32_t* first_of_label;   // optional (grouped runs): label -> sorted position of the cluster's first hit
+  label_map lm;               // label destinations (sharded runs)
 };
 
 #define TPX_PHASE(k)                                                         \
@@ -960,7 +982,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         a.open_hits[oh] = (uint32_t)pos;
       } else {
         a.parent_g[pos] = kSentinel;
-        a.labels[rq[q].idx] = label;
+        store_label(a.labels, a.n_owned, a.lm, rq[q].idx, label);
       }
       if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
     }

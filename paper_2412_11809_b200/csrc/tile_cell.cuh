@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         a.parent_g[pos] = (uint32_t)(t0 + r);
       } else {
         a.parent_g[pos] = kSentinel;
-        a.labels[tidx[q]] = label;
+        store_label(a.labels, a.n_owned, a.lm, tidx[q], label);
       }
     }
   }

@@ -22,7 +22,6 @@
 #include "group.cuh"
 #include "variant.cuh"
 #include "scan.cuh"
-#include "shard.cuh"
 #include "sort.cuh"
 #include "sort_window.cuh"
 #include "tile_cc.cuh"
@@ -185,7 +184,7 @@ static int exclusive_scan(tpx_cluster* c, const uint32_t* in, uint64_t n, uint32
 }
 
 template <typename KeyT>
-static int radix_sort(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t toa_min, int passes, char* ws,
+static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min, int passes, char* ws,
                       const layout& L, uint32_t** perm_out, cudaStream_t s) {
   KeyT* k0 = (KeyT*)(ws + L.keys0);
   KeyT* k1 = (KeyT*)(ws + L.keys1);
@@ -232,7 +231,7 @@ static int radix_sort(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint64_t 
 }
 
 struct run_ptrs {
-  const tpx_hit* hits;
+  hit_src hits;
   uint64_t n;
   uint64_t n_owned;
   uint32_t* labels;
@@ -244,6 +243,10 @@ struct run_ptrs {
   bool dense;   // tile configuration chosen by the density probe
   uint32_t sort_T = kWSortTile;  // output tile of the sort that produced S (its borders are verified)
   bool column;  // legacy column-bucket sparse kernel (TPX_TILE_COLUMN, comparison only)
+  // sharded runs (sharded.cuh): labels written as global indices into two
+  // arrays, emission deferred until the boundary clusters are merged
+  label_map lm = {};
+  bool defer_emit = false;
 };
 
 // The header is initialised by a kernel, not by an H2D copy of a host
@@ -303,6 +306,9 @@ static int sort_global(tpx_cluster* c, const run_ptrs& r) {
   return TPX_OK;
 }
 
+static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* removed_out,
+                       unsigned long long* n_removed);
+
 // Tile clustering + border merge + ordered emission on a sorted S.
 static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   char* ws = r.ws;
@@ -318,8 +324,6 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   uint2* overflow = (uint2*)(ws + L.overflow);
   uint2* pairs = (uint2*)(ws + L.pairs);
   uint32_t* bitmap = (uint32_t*)(ws + L.bitmap);
-  uint32_t* wcnt = (uint32_t*)(ws + L.wcnt);
-  uint32_t* partials = (uint32_t*)(ws + L.partials);
 
   if (c->profiling) cudaEventRecord(c->ev[1], r.s);
   tile_args a;
@@ -344,6 +348,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.phase_cycles = c->profiling >= 2 ? hdr->phase_cycles : nullptr;
   a.tile_meta = nullptr;
   a.first_of_label = c->want_first ? (uint32_t*)(ws + L.minidx) : nullptr;
+  a.lm = r.lm;
   if (r.dense)
     k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
                             r.s>>>(a);
@@ -370,18 +375,35 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   k_merge_open<<<kListGrid, kListThreads, 0, r.s>>>(open_comps, hdr, parent_g, slot_of, stage);
   TPX_LAUNCHED(c);
   k_open_labels<<<kListGrid, kListThreads, 0, r.s>>>(S, open_hits, open_comps, hdr, parent_g, slot_of, stage,
-                                                     r.labels, bitmap, (uint32_t)r.n_owned, a.first_of_label);
+                                                     r.labels, bitmap, (uint32_t)r.n_owned, a.first_of_label, r.lm);
   TPX_LAUNCHED(c);
+  if (r.defer_emit) return TPX_OK;  // sharded: emit_sorted() after the boundary merge
+  return emit_sorted(c, r, nullptr, nullptr);
+}
+
+// A6 + A7 emission: ordinal of every label bit, records copied in label
+// order.  removed_out (sharded runs): records whose label bit was cleared by
+// the boundary merge are appended there (global labels) instead.
+static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* removed_out,
+                       unsigned long long* n_removed) {
+  char* ws = r.ws;
+  const layout& L = r.L;
+  dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
+  const tpx_cluster_features* stage = (const tpx_cluster_features*)(ws + L.stage);
+  const uint32_t* comp_count = (const uint32_t*)(ws + L.comp_count);
+  uint32_t* bitmap = (uint32_t*)(ws + L.bitmap);
+  uint32_t* wcnt = (uint32_t*)(ws + L.wcnt);
+  uint32_t* partials = (uint32_t*)(ws + L.partials);
 
   if (c->profiling) cudaEventRecord(c->ev[3], r.s);
   k_popc<<<grid_for(L.nwords, 256), 256, 0, r.s>>>(bitmap, L.nwords, wcnt);
   TPX_LAUNCHED(c);
   int rc = exclusive_scan(c, wcnt, L.nwords, wcnt, partials, (uint32_t*)&hdr->n_clusters, r.s);
   if (rc) return rc;
-  if (r.capacity) {
+  if (r.capacity || removed_out) {
     const uint32_t tile = r.dense ? tile_dense::kTile : r.column ? tile_sparse::kTile : cell_sparse::kTile;
     k_emit<<<kListGrid, kEmitThreads, 0, r.s>>>(stage, comp_count, n_tiles_of(r.n, tile), tile, bitmap, wcnt, r.feats,
-                                                r.capacity);
+                                                r.capacity, r.lm.own_off, removed_out, n_removed);
     TPX_LAUNCHED(c);
   }
   if (c->profiling) cudaEventRecord(c->ev[4], r.s);
@@ -572,6 +594,9 @@ static int run_variant(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uint32_t
   return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
 }
 
+static int run_core(tpx_cluster* c, run_ptrs& r);
+static void finish_stats(tpx_cluster* c);
+
 extern "C" {
 
 int tpx_abi_version(void) { return TPX_ABI_VERSION; }
@@ -580,7 +605,9 @@ const char* tpx_status_string(int s) {
   switch (s) {
     case TPX_OK: return "ok";
     case TPX_ERR_INVALID_ARG: return "invalid argument";
-    case TPX_ERR_UNSUPPORTED: return "unsupported for this variant (sharded runs and streams: variant (iii)(a) only)";
+    case TPX_ERR_UNSUPPORTED:
+      return "unsupported (variant (iii)(a) only for sharded runs and streams; sharded runs: sensor width <= 1024, "
+             "no rank-skipping edge, halo <= TPX_SHARD_HALO_CAP)";
     case TPX_ERR_COORD_RANGE: return "hit coordinate outside the sensor or toa >= 2^48";
     case TPX_ERR_TOO_MANY_HITS: return "too many hits (n must be < 2^32 - 1)";
     case TPX_ERR_CAPACITY: return "feature capacity too small (n_clusters_out holds the required count)";
@@ -678,7 +705,7 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   r.L = make_layout(n);
   if (workspace_bytes < r.L.total) return TPX_ERR_OOM;
   if (ensure_cuda(c)) return TPX_ERR_CUDA;
-  r.hits = hits;
+  r.hits = hit_src(hits);
   r.n = n;
   r.n_owned = n_owned;
   r.labels = labels_out;
@@ -686,10 +713,26 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
   r.capacity = capacity;
   r.ws = (char*)workspace;
   r.s = (cudaStream_t)stream;
+  int rc = run_core(c, r);
+  if (rc) return rc;
+  const uint64_t k = c->stats.n_clusters;
+  *n_clusters_out = k;
+  return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
+}
+
+}  // extern "C"
+
+// Sort attempts + clustering + (unless r.defer_emit) emission for a prepared
+// run; fills c->stats (n_clusters from the emission's scan).  Deferred runs
+// (sharded.cuh) return after the clustering kernels are queued, without a
+// host synchronisation: the caller finishes with emit_sorted().
+static int run_core(tpx_cluster* c, run_ptrs& r) {
+  const uint64_t n = r.n;
   srec* S = (srec*)(r.ws + r.L.S);
   dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
 
   int rc;
+  const hit_src hits = r.hits;
   // attempts 0 / 1 / 2: windowed sort with D = 1024 / 2560 / 3072;
   // attempt 3: global radix sort; attempt 4: global union-find pipeline
   // (internal fallback)
@@ -776,8 +819,10 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     const bool big_sensor =
         c->width > (uint32_t)kBuckets || (uint64_t)c->width * c->height + c->width > kMaxTilePixels;
     c->bitmap_valid = !(attempt == kRadixAttempt + 1 || big_sensor);
+    if (r.defer_emit && !c->bitmap_valid) return TPX_ERR_UNSUPPORTED;  // sharded: tile path only
     rc = c->bitmap_valid ? cluster_sorted(c, r) : cluster_global(c, r);
     if (rc) return rc;
+    if (r.defer_emit) return TPX_OK;
     if ((rc = read_header(c, r))) return rc;
     const dev_hdr& h = *c->host_hdr;
     if (h.err & 1u) return TPX_ERR_COORD_RANGE;
@@ -794,9 +839,14 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
     }
     break;
   }
+  finish_stats(c);
+  return TPX_OK;
+}
+
+// Counters of the last run from the (synchronised) host header.
+static void finish_stats(tpx_cluster* c) {
   const dev_hdr& h = *c->host_hdr;
   const uint64_t k = (uint32_t)h.n_clusters;  // low word written by the scan
-  *n_clusters_out = k;
   c->stats.n_clusters = k;
   c->stats.cross_pairs = h.n_pairs;
   c->stats.open_hits = h.n_open_hits;
@@ -810,8 +860,10 @@ int tpx_cluster_run_partial(tpx_cluster* c, const tpx_hit* hits, uint64_t n, uin
       c->stats.stage_ms[i] = ms;
     }
   }
-  return k > capacity ? TPX_ERR_CAPACITY : TPX_OK;
 }
+
+extern "C" {
+
 
 // G4 fallback: stable global LSD radix sort of (block index, input index)
 // on ceil(log2 k) bits.
@@ -1001,279 +1053,5 @@ int tpx_cluster_centroids(const tpx_cluster_features* features, uint64_t k, doub
 
 }  // extern "C"
 
-// ============================================================ sharded path
-namespace {
-
-#define TPX_K(...)                                                                  \
-  do {                                                                              \
-    __VA_ARGS__;                                                                    \
-    cudaError_t e_ = cudaGetLastError();                                            \
-    if (e_ != cudaSuccess) {                                                        \
-      fprintf(stderr, "tpx_shard: launch failed: %s\n", cudaGetErrorString(e_));    \
-      return TPX_ERR_CUDA;                                                          \
-    }                                                                               \
-  } while (0)
-
-int scan_u32(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* partials, uint32_t* total, cudaStream_t s) {
-  const uint32_t tiles = n_tiles_of(n, kScanTile);
-  TPX_K(k_scan_reduce<<<tiles, kScanThreads, 0, s>>>(in, n, partials));
-  TPX_K(k_scan_partials<<<1, kScanThreads, 0, s>>>(partials, tiles, total));
-  TPX_K(k_scan_down<<<tiles, kScanThreads, 0, s>>>(in, n, partials, out));
-  return TPX_OK;
-}
-
-size_t scan_partials_bytes(uint64_t n) {
-  const uint32_t rt = n_tiles_of(n, kRadixTile);
-  uint32_t st = n_tiles_of((uint64_t)rt * kRadixBins, kScanTile);
-  st = st > n_tiles_of(n, kScanTile) ? st : n_tiles_of(n, kScanTile);
-  return (size_t)st * 4 + 64;
-}
-
-// Stable LSD radix sort of n u32 keys with u32 payload (4 passes, result in place).
-int sort_u32(uint32_t* keys, uint32_t* vals, uint64_t n, uint32_t* tk, uint32_t* tv, uint32_t* hist,
-             uint32_t* partials, cudaStream_t s) {
-  const uint32_t tiles = n_tiles_of(n, kRadixTile);
-  uint32_t *k0 = keys, *k1 = tk, *v0 = vals, *v1 = tv;
-  for (int p = 0; p < 4; ++p) {
-    TPX_K(k_radix_hist<uint32_t, false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, n, 0, 8 * p, hist, tiles));
-    int rc = scan_u32(hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s);
-    if (rc) return rc;
-    TPX_K(k_radix_scatter_tile<false><<<tiles, kRadixThreads, 0, s>>>(nullptr, k0, v0, n, 0, 8 * p, hist, tiles, k1,
-                                                                     v1));
-    uint32_t* t = k0;
-    k0 = k1;
-    k1 = t;
-    t = v0;
-    v0 = v1;
-    v1 = t;
-  }
-  return TPX_OK;  // 4 swaps: result is back in keys / vals
-}
-
-size_t sort_u32_ws(uint64_t n) {
-  return align256(n * 4) * 2 + align256((size_t)n_tiles_of(n, kRadixTile) * kRadixBins * 4) +
-         align256(scan_partials_bytes(n));
-}
-
-}  // namespace
-
-extern "C" {
-
-int tpx_shard_toa_range(const tpx_hit* hits, uint64_t n, uint64_t* minmax, void* stream) {
-  if (!minmax || (n && !hits)) return TPX_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  TPX_K(k_range_init<<<1, 1, 0, s>>>((unsigned long long*)minmax));
-  if (n) TPX_K(k_toa_range<<<grid_for(n, 256), 256, 0, s>>>(hits, n, (unsigned long long*)minmax));
-  return TPX_OK;
-}
-
-int tpx_shard_select_workspace_bytes(uint64_t n, size_t* bytes) {
-  if (!bytes) return TPX_ERR_INVALID_ARG;
-  *bytes = align256(n * 4) * 2 + align256(scan_partials_bytes(n)) + 256;
-  return TPX_OK;
-}
-
-int tpx_shard_select_halo(const tpx_hit* hits, uint64_t n, uint64_t toa_limit, tpx_hit* halo_out,
-                          uint32_t* idx_out, uint64_t* count, void* workspace, size_t workspace_bytes,
-                          void* stream) {
-  size_t need = 0;
-  tpx_shard_select_workspace_bytes(n, &need);
-  if (!count || workspace_bytes < need || (n && (!hits || !halo_out || !idx_out || !workspace)))
-    return TPX_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(count, 0, 8, s) != cudaSuccess) return TPX_ERR_CUDA;
-  if (n == 0) return TPX_OK;
-  char* ws = (char*)workspace;
-  uint32_t* flags = (uint32_t*)ws;
-  uint32_t* ord = (uint32_t*)(ws + align256(n * 4));
-  uint32_t* partials = (uint32_t*)(ws + 2 * align256(n * 4));
-  TPX_K(k_halo_flags<<<grid_for(n, 256), 256, 0, s>>>(hits, n, toa_limit, flags));
-  int rc = scan_u32(flags, n, ord, partials, (uint32_t*)count, s);
-  if (rc) return rc;
-  TPX_K(k_halo_scatter<<<grid_for(n, 256), 256, 0, s>>>(hits, n, flags, ord, halo_out, idx_out));
-  return TPX_OK;
-}
-
-int tpx_shard_translate_labels(uint32_t* labels, uint64_t n, uint64_t n_owned, uint64_t own_offset,
-                               const uint32_t* halo_idx, uint64_t next_offset, void* stream) {
-  if (n == 0) return TPX_OK;
-  if (!labels || n_owned > n || (n > n_owned && !halo_idx)) return TPX_ERR_INVALID_ARG;
-  TPX_K(k_translate<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(labels, n, n_owned, own_offset, halo_idx,
-                                                                         next_offset));
-  return TPX_OK;
-}
-
-int tpx_shard_offset_labels(tpx_cluster_features* features, uint64_t k, uint64_t offset, void* stream) {
-  if (k == 0) return TPX_OK;
-  if (!features || offset >= 0xffffffffull) return TPX_ERR_INVALID_ARG;
-  TPX_K(k_offset_labels<<<grid_for(k, 256), 256, 0, (cudaStream_t)stream>>>(features, k, (uint32_t)offset));
-  return TPX_OK;
-}
-
-int tpx_shard_gather_labels(const uint32_t* labels, const uint32_t* idx, uint64_t count, uint32_t* out,
-                            void* stream) {
-  if (count == 0) return TPX_OK;
-  if (!labels || !idx || !out) return TPX_ERR_INVALID_ARG;
-  TPX_K(k_gather_u32<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(labels, idx, count, out));
-  return TPX_OK;
-}
-
-int tpx_shard_make_pairs(const uint32_t* a, const uint32_t* b, uint64_t count, uint32_t* pairs_out,
-                         uint64_t* n_pairs, void* stream) {
-  if (!n_pairs || (count && (!a || !b || !pairs_out))) return TPX_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(n_pairs, 0, 8, s) != cudaSuccess) return TPX_ERR_CUDA;
-  if (count)
-    TPX_K(k_make_pairs<<<grid_for(count, 256), 256, 0, s>>>(a, b, count, (uint2*)pairs_out,
-                                                            (unsigned long long*)n_pairs));
-  return TPX_OK;
-}
-
-int tpx_shard_union_workspace_bytes(uint64_t n_pairs, size_t* bytes) {
-  if (!bytes) return TPX_ERR_INVALID_ARG;
-  const uint64_t m = 2 * n_pairs;
-  *bytes = align256(m * 4) * 6 + sort_u32_ws(m) + 512;
-  return TPX_OK;
-}
-
-int tpx_shard_union_pairs(const uint32_t* pairs, uint64_t n_pairs, uint32_t* map_keys, uint32_t* map_vals,
-                          uint64_t* n_map, void* workspace, size_t workspace_bytes, void* stream) {
-  size_t need = 0;
-  tpx_shard_union_workspace_bytes(n_pairs, &need);
-  if (!n_map || workspace_bytes < need || (n_pairs && (!pairs || !map_keys || !map_vals || !workspace)))
-    return TPX_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(n_map, 0, 8, s) != cudaSuccess) return TPX_ERR_CUDA;
-  if (n_pairs == 0) return TPX_OK;
-  const uint64_t m = 2 * n_pairs;
-  char* ws = (char*)workspace;
-  size_t off = 0;
-  auto take = [&](size_t b) {
-    char* p = ws + off;
-    off += align256(b);
-    return p;
-  };
-  uint32_t* keys = (uint32_t*)take(m * 4);
-  uint32_t* vals = (uint32_t*)take(m * 4);
-  uint32_t* flags = (uint32_t*)take(m * 4);
-  uint32_t* ord = (uint32_t*)take(m * 4);
-  uint32_t* parent = (uint32_t*)take(m * 4);
-  uint32_t* tmp = (uint32_t*)take(m * 4);
-  uint32_t* tk = (uint32_t*)take(m * 4);
-  uint32_t* tv = (uint32_t*)take(m * 4);
-  uint32_t* hist = (uint32_t*)take((size_t)n_tiles_of(m, kRadixTile) * kRadixBins * 4);
-  uint32_t* partials = (uint32_t*)take(scan_partials_bytes(m));
-  (void)tmp;
-  if (cudaMemcpyAsync(keys, pairs, m * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return TPX_ERR_CUDA;
-  int rc = sort_u32(keys, vals, m, tk, tv, hist, partials, s);
-  if (rc) return rc;
-  TPX_K(k_unique_flags<<<grid_for(m, 256), 256, 0, s>>>(keys, m, flags));
-  rc = scan_u32(flags, m, ord, partials, (uint32_t*)n_map, s);
-  if (rc) return rc;
-  TPX_K(k_unique_scatter<<<grid_for(m, 256), 256, 0, s>>>(keys, m, flags, ord, map_keys, parent));
-  TPX_K(k_pair_union<<<grid_for(n_pairs, 256), 256, 0, s>>>((const uint2*)pairs, n_pairs, map_keys,
-                                                            (const uint32_t*)n_map, parent));
-  TPX_K(k_pair_finals<<<grid_for(m, 256), 256, 0, s>>>(map_keys, (const uint32_t*)n_map, parent, map_vals));
-  return TPX_OK;
-}
-
-int tpx_shard_relabel(uint32_t* labels, uint64_t n, const uint32_t* map_keys, const uint32_t* map_vals,
-                      const uint64_t* n_map, void* stream) {
-  if (n == 0) return TPX_OK;
-  if (!labels || !map_keys || !map_vals || !n_map) return TPX_ERR_INVALID_ARG;
-  TPX_K(k_relabel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(labels, n, map_keys, map_vals,
-                                                                       (const unsigned long long*)n_map));
-  return TPX_OK;
-}
-
-int tpx_shard_split_workspace_bytes(uint64_t k, size_t* bytes) {
-  if (!bytes) return TPX_ERR_INVALID_ARG;
-  *bytes = align256(k * 4) * 2 + align256(scan_partials_bytes(k)) + 256;
-  return TPX_OK;
-}
-
-int tpx_shard_split_features(const tpx_cluster_features* feats, uint64_t k, const uint32_t* map_keys,
-                             const uint32_t* map_vals, const uint64_t* n_map, tpx_cluster_features* kept_out,
-                             uint64_t* n_kept, tpx_cluster_features* partials_out, uint64_t* n_partials,
-                             void* workspace, size_t workspace_bytes, void* stream) {
-  size_t need = 0;
-  tpx_shard_split_workspace_bytes(k, &need);
-  if (!n_kept || !n_partials || workspace_bytes < need ||
-      (k && (!feats || !map_keys || !map_vals || !n_map || !kept_out || !partials_out || !workspace)))
-    return TPX_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(n_kept, 0, 8, s) != cudaSuccess || cudaMemsetAsync(n_partials, 0, 8, s) != cudaSuccess)
-    return TPX_ERR_CUDA;
-  if (k == 0) return TPX_OK;
-  char* ws = (char*)workspace;
-  uint32_t* keep = (uint32_t*)ws;
-  uint32_t* ord = (uint32_t*)(ws + align256(k * 4));
-  uint32_t* partials = (uint32_t*)(ws + 2 * align256(k * 4));
-  TPX_K(k_split_flags<<<grid_for(k, 256), 256, 0, s>>>(feats, k, map_keys, map_vals, (const unsigned long long*)n_map,
-                                                       keep, partials_out, (unsigned long long*)n_partials));
-  int rc = scan_u32(keep, k, ord, partials, (uint32_t*)n_kept, s);
-  if (rc) return rc;
-  TPX_K(k_compact_records<<<grid_for(k, 256), 256, 0, s>>>(feats, k, keep, ord, kept_out));
-  return TPX_OK;
-}
-
-int tpx_shard_fold_workspace_bytes(uint64_t n_partials, size_t* bytes) {
-  if (!bytes) return TPX_ERR_INVALID_ARG;
-  const uint64_t q = n_partials ? n_partials : 1;
-  *bytes = align256(q * 4) * 4 + align256(q * 64) + sort_u32_ws(q) + 512;
-  return TPX_OK;
-}
-
-int tpx_shard_fold_features(const tpx_cluster_features* kept, uint64_t n_kept, const tpx_cluster_features* partials,
-                            uint64_t n_partials, uint64_t label_lo, uint64_t label_hi, tpx_cluster_features* out,
-                            uint64_t capacity, uint64_t* n_out, void* workspace, size_t workspace_bytes,
-                            void* stream) {
-  size_t need = 0;
-  tpx_shard_fold_workspace_bytes(n_partials, &need);
-  if (!n_out || workspace_bytes < need || !workspace || (n_kept && !kept) || (n_partials && !partials) ||
-      (capacity && !out))
-    return TPX_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  const uint64_t q = n_partials ? n_partials : 1;
-  char* ws = (char*)workspace;
-  size_t off = 0;
-  auto take = [&](size_t b) {
-    char* p = ws + off;
-    off += align256(b);
-    return p;
-  };
-  uint32_t* keys = (uint32_t*)take(q * 4);
-  uint32_t* vals = (uint32_t*)take(q * 4);
-  uint32_t* head = (uint32_t*)take(q * 4);
-  uint32_t* ord = (uint32_t*)take(q * 4);
-  tpx_cluster_features* merged = (tpx_cluster_features*)take(q * 64);
-  uint32_t* tk = (uint32_t*)take(q * 4);
-  uint32_t* tv = (uint32_t*)take(q * 4);
-  uint32_t* hist = (uint32_t*)take((size_t)n_tiles_of(q, kRadixTile) * kRadixBins * 4);
-  uint32_t* sp = (uint32_t*)take(scan_partials_bytes(q));
-  unsigned long long* cnt = (unsigned long long*)take(16);  // [0] in-block partials, [1] merged count (u32 low)
-  if (cudaMemsetAsync(cnt, 0, 16, s) != cudaSuccess || cudaMemsetAsync(keys, 0xff, q * 4, s) != cudaSuccess ||
-      cudaMemsetAsync(head, 0, q * 4, s) != cudaSuccess)
-    return TPX_ERR_CUDA;
-  if (n_partials) {
-    TPX_K(k_fold_keys<<<grid_for(n_partials, 256), 256, 0, s>>>(partials, n_partials, label_lo, label_hi, keys, vals,
-                                                                cnt));
-    int rc = sort_u32(keys, vals, q, tk, tv, hist, sp, s);
-    if (rc) return rc;
-    TPX_K(k_run_heads<<<grid_for(q, 256), 256, 0, s>>>(keys, cnt, head));
-    rc = scan_u32(head, q, ord, sp, (uint32_t*)(cnt + 1), s);
-    if (rc) return rc;
-    TPX_K(k_fold_runs<<<grid_for(q, 256), 256, 0, s>>>(partials, keys, vals, cnt, head, ord, merged));
-  }
-  TPX_K(k_merge_records<<<grid_for(n_kept + q, 256), 256, 0, s>>>(kept, n_kept, merged, (const uint32_t*)(cnt + 1),
-                                                                  out, capacity));
-  unsigned long long h[2];
-  if (cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
-    return TPX_ERR_CUDA;
-  *n_out = n_kept + (uint32_t)h[1];
-  return *n_out > capacity ? TPX_ERR_CAPACITY : TPX_OK;
-}
-
-}  // extern "C"
-
+#include "sharded.cuh"
 #include "stream.cuh"

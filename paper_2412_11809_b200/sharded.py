@@ -1,31 +1,29 @@
-"""ToA-sharded multi-GPU clustering (§3.2.3 l.117-119).
+"""ToA-sharded multi-GPU clustering: binding of ``tpx_cluster_run_sharded``.
 
-One process (or, for tests, one thread) per GPU.  Rank r owns the
-contiguous input-index block [o_r, o_r + n_r) of the t-ordered stream.  The
-protocol (every compute step is a device kernel behind the C ABI, ``ops``;
-every exchange is a collective on ``comm``):
+The whole protocol -- ranges, halo selection and exchange, boundary pairs,
+union, relabelling, partial records and their fold -- runs inside the C-ABI
+library (``csrc/sharded.cuh``, ``csrc/comm.cu``); this module only creates
+communicators and marshals arguments (§3.2.3
+l.117-119 temporal splitting, §4 l.173 border stitching).
 
-  1. all-gather block sizes -> offsets; all-gather [minToA, maxToA] and check
-     that no edge can skip a rank (minToA(r+2) > maxToA(r) + dt_max);
-  2. rank r+1 selects its hits with toa <= maxToA(r) + dt_max (the forward
-     halo of rank r) and sends them (and their block positions) to rank r;
-  3. each rank clusters [owned | halo] with ``run_partial`` (features only
-     from owned hits), translates labels to global input indices;
-  4. rank r+1 sends back its own labels of the hits it lent; the halo hits'
-     two labels form boundary pairs; all ranks all-gather the pairs and run
-     the same union pass (smallest label wins);
-  5. relabel owned hits; records of merged clusters become partials, are
-     all-gathered, and each owner folds those whose final label it owns.
-
-Concatenating the ranks' labels and records in rank order gives exactly the
-single-GPU result (tests/test_gpu_sharded.py checks this bit for bit).
+Communicators (``tpx_comm``):
+  * :class:`NcclComm` -- the product path: a library-owned NCCL communicator
+    (one process per GPU, NVLink / NVSwitch), bootstrapped over a
+    torch.distributed process group (rank 0's ``tpx_nccl_unique_id`` is
+    broadcast, every rank calls ``tpx_nccl_comm_init``).
+  * :class:`HostComm` -- host-callback transport for functional runs where
+    NCCL cannot be used (in-process virtual ranks: :class:`ThreadAdapter`;
+    gloo process groups, e.g. several ranks sharing one GPU:
+    :class:`TorchAdapter`).  The library stages device buffers through
+    pinned host memory and calls back into these adapters.
 """
 from __future__ import annotations
 
+import ctypes
 import threading
 from dataclasses import dataclass
 
-import numpy as np
+import paper_2412_11809_b200 as _tpx
 
 HIT_BYTES = 16
 FEAT_BYTES = 64
@@ -35,54 +33,104 @@ class ShardError(RuntimeError):
     pass
 
 
-# ---------------------------------------------------------------- communicators
-class TorchComm:
-    """torch.distributed process group (NCCL on GPUs, gloo on CPU).
+# ------------------------------------------------------------ communicators
+class _Comm:
+    _h = None
 
-    ``staged=True`` routes device tensors through host memory for every
-    collective -- a gloo process group on GPU ranks (functional runs of the
-    multi-process path where NCCL is unavailable, e.g. several ranks sharing
-    one GPU); the NVLink path is NCCL with staged=False."""
+    @property
+    def handle(self):
+        return self._h
 
-    def __init__(self, group=None, staged: bool = False):
-        import torch.distributed as dist
+    def rank_world(self):
+        r, w = ctypes.c_int(0), ctypes.c_int(0)
+        _tpx._check(_tpx._comm_rank(self._h, ctypes.byref(r), ctypes.byref(w)), "tpx_comm_rank")
+        return r.value, w.value
 
-        self.dist = dist
-        self.group = group
-        self.staged = staged
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
+    def close(self):
+        if self._h:
+            _tpx._comm_destroy(self._h)
+            self._h = None
 
-    def allgather(self, t):
-        """All-gather equal-shape tensors -> list (rank order)."""
-        src = t.contiguous().cpu() if self.staged else t.contiguous()
-        out = [src.new_empty(src.shape) for _ in range(self.world)]
-        self.dist.all_gather(out, src, group=self.group)
-        return [o.to(t.device) for o in out] if self.staged else out
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
-    def exchange(self, send_to, send_tensors, recv_from, recv_tensors):
-        """Point-to-point: send a list to one peer, receive a list from another."""
-        ops = []
-        P2POp, isend, irecv = self.dist.P2POp, self.dist.isend, self.dist.irecv
-        sends = [t.contiguous().cpu() if self.staged else t.contiguous() for t in send_tensors]
-        recvs = [t.new_empty(t.shape, device="cpu") if self.staged else t for t in recv_tensors]
-        if send_to is not None:
-            ops += [P2POp(isend, t, send_to, self.group) for t in sends]
-        if recv_from is not None:
-            ops += [P2POp(irecv, t, recv_from, self.group) for t in recvs]
-        if ops:
-            for w in self.dist.batch_isend_irecv(ops):
-                w.wait()
-        if self.staged and recv_from is not None:
-            for dst, src in zip(recv_tensors, recvs):
-                dst.copy_(src)
 
-    def barrier(self):
-        self.dist.barrier(group=self.group)
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL bootstrap id (``tpx_nccl_unique_id``), created on rank 0."""
+    uid = ctypes.create_string_buffer(128)
+    _tpx._check(_tpx._nccl_unique_id(uid), "tpx_nccl_unique_id")
+    return uid.raw
+
+
+class NcclComm(_Comm):
+    """Library-owned NCCL communicator on the current CUDA device.
+
+    ``NcclComm()`` bootstraps over the default torch.distributed process group
+    (or ``group``): rank 0's unique id is broadcast, every rank calls
+    ``tpx_nccl_comm_init``.  ``NcclComm(rank=r, world=w, uid=...)`` takes an id
+    distributed by other means (``world=1`` needs none)."""
+
+    def __init__(self, group=None, rank: int | None = None, world: int | None = None, uid: bytes | None = None):
+        if rank is None:
+            import torch.distributed as dist
+
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            obj = [nccl_unique_id() if rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            uid = obj[0]
+        elif uid is None:
+            if world != 1:
+                raise ShardError("NcclComm(rank, world): a unique id is needed for world > 1")
+            uid = nccl_unique_id()
+        h = _tpx._vp()
+        _tpx._check(_tpx._nccl_comm_init(int(rank), int(world), uid, ctypes.byref(h)), "tpx_nccl_comm_init")
+        self._h = h
+
+
+class HostComm(_Comm):
+    """Host-callback transport around an adapter with ``rank``, ``world``,
+    ``allgather(data: bytes) -> list[bytes]`` (rank order) and
+    ``sendrecv(to, data, frm, nbytes) -> bytes`` (-1 = no peer)."""
+
+    def __init__(self, adapter):
+        self.adapter = adapter
+
+        def allgather(_user, send, recv, nbytes):
+            try:
+                parts = adapter.allgather(ctypes.string_at(send, nbytes) if nbytes else b"")
+                buf = b"".join(parts)
+                ctypes.memmove(recv, buf, len(buf))
+                return 0
+            except Exception:  # surfaced to the library as a transport error
+                return 1
+
+        def sendrecv(_user, to, send, send_bytes, frm, recv, recv_bytes):
+            try:
+                data = ctypes.string_at(send, send_bytes) if (to >= 0 and send_bytes) else b""
+                got = adapter.sendrecv(to, data, frm, recv_bytes)
+                if frm >= 0 and recv_bytes:
+                    ctypes.memmove(recv, got, recv_bytes)
+                return 0
+            except Exception:
+                return 1
+
+        # keep the callback objects alive as long as the communicator
+        self._cb = (_tpx.ALLGATHER_FN(allgather), _tpx.SENDRECV_FN(sendrecv))
+        h = _tpx._vp()
+        _tpx._check(_tpx._comm_create_host(adapter.rank, adapter.world, self._cb[0], self._cb[1], None,
+                                           ctypes.byref(h)), "tpx_comm_create_host")
+        self._h = h
+
+    def selftest(self, nbytes: int = 4096) -> int:
+        return _tpx._comm_selftest(self._h, nbytes)
 
 
 class ThreadGroup:
-    """Shared state for ThreadComm: N virtual ranks as threads of one process."""
+    """N virtual ranks as threads of one process (shared slots + barrier)."""
 
     def __init__(self, world: int):
         self.world = world
@@ -92,252 +140,127 @@ class ThreadGroup:
         self.lock = threading.Lock()
 
 
-class ThreadComm:
-    """In-process communicator (virtual ranks as threads): same protocol, same
-    kernels, collectives replaced by copies -- the multi-rank path on one GPU."""
-
-    def __init__(self, group: ThreadGroup, rank: int, device=None):
+class ThreadAdapter:
+    def __init__(self, group: ThreadGroup, rank: int):
         self.g, self.rank, self.world = group, rank, group.world
-        self.device = device
 
-    def allgather(self, t):
-        import torch
-
-        if t.is_cuda:
-            torch.cuda.current_stream(t.device).synchronize()
+    def allgather(self, data: bytes):
         self.g.barrier.wait()
-        self.g.slots[self.rank] = t.detach().clone()
+        self.g.slots[self.rank] = data
         self.g.barrier.wait()
-        out = [s.to(t.device) for s in self.g.slots]
+        out = list(self.g.slots)
         self.g.barrier.wait()
         return out
 
-    def exchange(self, send_to, send_tensors, recv_from, recv_tensors):
-        import torch
-
-        if send_to is not None:
-            for t in send_tensors:
-                if t.is_cuda:
-                    torch.cuda.current_stream(t.device).synchronize()
+    def sendrecv(self, to, data, frm, nbytes):
+        if to >= 0:
             with self.g.lock:
-                self.g.mail[(self.rank, send_to)] = [t.detach().clone() for t in send_tensors]
+                self.g.mail[(self.rank, to)] = data
         self.g.barrier.wait()
-        if recv_from is not None:
+        got = b""
+        if frm >= 0:
             with self.g.lock:
-                got = self.g.mail.pop((recv_from, self.rank))
-            for dst, src in zip(recv_tensors, got):
-                dst.copy_(src.to(dst.device))
+                got = self.g.mail.pop((frm, self.rank))
         self.g.barrier.wait()
-
-    def barrier(self):
-        self.g.barrier.wait()
+        return got
 
 
-# ----------------------------------------------------------------------- ops
-class CudaOps:
-    """Compute steps as C-ABI kernel calls on CUDA tensors (the product path)."""
+class TorchAdapter:
+    """torch.distributed on CPU tensors (gloo)."""
 
-    def __init__(self, dt_max: int, width: int = 256, height: int = 256):
+    def __init__(self, group=None):
         import torch
+        import torch.distributed as dist
 
-        import paper_2412_11809_b200 as tpx
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
 
-        self.torch, self.tpx = torch, tpx
-        self.dt = int(dt_max)
-        self.clusterer = tpx.Clusterer(dt_max, width, height)
-        self.device = torch.device("cuda", torch.cuda.current_device())
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
 
-    def _ws(self, nbytes):
-        return self.torch.empty(max(int(nbytes), 256), dtype=self.torch.uint8, device=self.device)
+    def allgather(self, data: bytes):
+        t = self.torch.frombuffer(bytearray(data), dtype=self.torch.uint8) if data else \
+            self.torch.empty(0, dtype=self.torch.uint8)
+        out = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.numpy().tobytes() for o in out]
 
-    def _u64(self, n=1):
-        return self.torch.zeros(n, dtype=self.torch.int64, device=self.device)
-
-    def toa_range(self, hits, n):
-        mm = self._u64(2)
-        self.tpx._check(self.tpx._shard_toa_range(hits.data_ptr() if n else None, n, mm.data_ptr(),
-                                                  self.tpx._stream_handle(None)), "tpx_shard_toa_range")
-        return mm
-
-    def select_halo(self, hits, n, toa_limit):
-        tpx = self.tpx
-        ws = self._ws(tpx._size_query(tpx._shard_select_ws, n))
-        halo = self.torch.empty((max(n, 1), HIT_BYTES), dtype=self.torch.uint8, device=self.device)
-        idx = self.torch.empty(max(n, 1), dtype=self.torch.int32, device=self.device)
-        cnt = self._u64()
-        tpx._check(tpx._shard_select(hits.data_ptr() if n else None, n, int(toa_limit), halo.data_ptr(),
-                                     idx.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(),
-                                     tpx._stream_handle(None)), "tpx_shard_select_halo")
-        c = int(cnt.item())
-        return halo[:c].contiguous(), idx[:c].contiguous(), c
-
-    def cluster_partial(self, hits, n, n_owned):
-        labels, feats, k = self.clusterer.run_partial(hits, n, n_owned)
-        return labels, feats, k
-
-    def translate(self, labels, n, n_owned, own_off, halo_idx, next_off):
-        tpx = self.tpx
-        tpx._check(tpx._shard_translate(labels.data_ptr(), n, n_owned, own_off,
-                                        halo_idx.data_ptr() if halo_idx.numel() else None, next_off,
-                                        tpx._stream_handle(None)), "tpx_shard_translate_labels")
-
-    def offset_feature_labels(self, feats, k, off):
-        tpx = self.tpx
-        tpx._check(tpx._shard_offset(feats.data_ptr() if k else None, k, int(off), tpx._stream_handle(None)),
-                   "tpx_shard_offset_labels")
-
-    def gather(self, labels, idx, c):
-        out = self.torch.empty(max(c, 1), dtype=self.torch.int32, device=self.device)
-        tpx = self.tpx
-        tpx._check(tpx._shard_gather(labels.data_ptr(), idx.data_ptr() if c else None, c, out.data_ptr(),
-                                     tpx._stream_handle(None)), "tpx_shard_gather_labels")
-        return out[:c]
-
-    def make_pairs(self, a, b, c):
-        pairs = self.torch.empty((max(c, 1), 2), dtype=self.torch.int32, device=self.device)
-        cnt = self._u64()
-        tpx = self.tpx
-        tpx._check(tpx._shard_pairs(a.data_ptr() if c else None, b.data_ptr() if c else None, c, pairs.data_ptr(),
-                                    cnt.data_ptr(), tpx._stream_handle(None)), "tpx_shard_make_pairs")
-        p = int(cnt.item())
-        return pairs[:p].contiguous(), p
-
-    def union_pairs(self, pairs, p):
-        tpx = self.tpx
-        ws = self._ws(tpx._size_query(tpx._shard_union_ws, p))
-        keys = self.torch.empty(max(2 * p, 1), dtype=self.torch.int32, device=self.device)
-        vals = self.torch.empty_like(keys)
-        nmap = self._u64()
-        tpx._check(tpx._shard_union(pairs.data_ptr() if p else None, p, keys.data_ptr(), vals.data_ptr(),
-                                    nmap.data_ptr(), ws.data_ptr(), ws.numel(), tpx._stream_handle(None)),
-                   "tpx_shard_union_pairs")
-        return keys, vals, nmap
-
-    def relabel(self, labels, n, mp):
-        keys, vals, nmap = mp
-        tpx = self.tpx
-        tpx._check(tpx._shard_relabel(labels.data_ptr(), n, keys.data_ptr(), vals.data_ptr(), nmap.data_ptr(),
-                                      tpx._stream_handle(None)), "tpx_shard_relabel")
-
-    def split(self, feats, k, mp):
-        keys, vals, nmap = mp
-        tpx, torch = self.tpx, self.torch
-        ws = self._ws(tpx._size_query(tpx._shard_split_ws, k))
-        kept = torch.empty((max(k, 1), FEAT_BYTES), dtype=torch.uint8, device=self.device)
-        part = torch.empty_like(kept)
-        nk, npart = self._u64(), self._u64()
-        tpx._check(tpx._shard_split(feats.data_ptr() if k else None, k, keys.data_ptr(), vals.data_ptr(),
-                                    nmap.data_ptr(), kept.data_ptr(), nk.data_ptr(), part.data_ptr(),
-                                    npart.data_ptr(), ws.data_ptr(), ws.numel(), tpx._stream_handle(None)),
-                   "tpx_shard_split_features")
-        a, b = int(nk.item()), int(npart.item())
-        return kept[:a], a, part[:b].contiguous(), b
-
-    def fold(self, kept, nk, partials, q, lo, hi, capacity):
-        tpx, torch = self.tpx, self.torch
-        ws = self._ws(tpx._size_query(tpx._shard_fold_ws, q))
-        out = torch.empty((max(capacity, 1), FEAT_BYTES), dtype=torch.uint8, device=self.device)
-        import ctypes
-
-        n_out = ctypes.c_uint64(0)
-        tpx._check(tpx._shard_fold(kept.data_ptr() if nk else None, nk, partials.data_ptr() if q else None, q,
-                                   int(lo), int(hi), out.data_ptr(), capacity, ctypes.byref(n_out), ws.data_ptr(),
-                                   ws.numel(), tpx._stream_handle(None)), "tpx_shard_fold_features")
-        return out[: n_out.value], n_out.value
-
-    # generic tensor helpers (device memory plumbing)
-    def empty_hits(self, n):
-        return self.torch.empty((max(n, 1), HIT_BYTES), dtype=self.torch.uint8, device=self.device)[:n]
-
-    def empty_u32(self, n):
-        return self.torch.empty(max(n, 1), dtype=self.torch.int32, device=self.device)[:n]
-
-    def empty_feats(self, n):
-        return self.torch.empty((max(n, 1), FEAT_BYTES), dtype=self.torch.uint8, device=self.device)[:n]
-
-    def cat(self, a, b):
-        return self.torch.cat([a.reshape(-1), b.reshape(-1)]).view(-1, a.shape[-1]) if a.dim() > 1 else \
-            self.torch.cat([a, b])
-
-    def scalar_tensor(self, values):
-        return self.torch.tensor(values, dtype=self.torch.int64, device=self.device)
-
-    def zeros_pairs(self, n):
-        return self.torch.zeros((n, 2), dtype=self.torch.int32, device=self.device)
-
-    def concat_rows(self, parts):
-        return self.torch.cat(parts).contiguous()
+    def sendrecv(self, to, data, frm, nbytes):
+        torch, dist = self.torch, self.dist
+        ops = []
+        if to >= 0 and data:
+            ops.append(dist.P2POp(dist.isend, torch.frombuffer(bytearray(data), dtype=torch.uint8), self._peer(to),
+                                  self.group))
+        rbuf = torch.empty(nbytes if frm >= 0 else 0, dtype=torch.uint8)
+        if frm >= 0 and nbytes:
+            ops.append(dist.P2POp(dist.irecv, rbuf, self._peer(frm), self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return rbuf.numpy().tobytes()
 
 
-# ------------------------------------------------------------------ protocol
+# ------------------------------------------------------------------ the run
 @dataclass
 class ShardResult:
-    labels: object        # this rank's labels (global input indices), n_r
-    features: object      # records whose label falls in this rank's block, ascending
+    labels: object      # this rank's labels (global input indices), n_r (int32 view of u32)
+    features: object    # records whose label falls in this rank's block, ascending (uint8 [k, 64])
     n_clusters: int
-    offset: int
+    offset: int         # o_r, first global index of this rank's block
     stats: dict
 
 
-def cluster_sharded(hits, dt_max: int, comm, ops) -> ShardResult:
-    """Run the sharded protocol for this rank's block ``hits`` ([n_r, 16] bytes)."""
-    G, r = comm.world, comm.rank
-    n = int(hits.shape[0]) if hits.dim() > 1 else int(hits.numel() // HIT_BYTES)
-    hits = hits.reshape(n, HIT_BYTES) if n else hits
-    sizes = [int(t[0].item()) for t in comm.allgather(ops.scalar_tensor([n]))]
-    if min(sizes) == 0:
-        raise ShardError("every rank needs at least one hit")
-    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    if offs[-1] >= 2**31:
-        raise ShardError("sharded path supports < 2^31 hits in total")
-    o_r = int(offs[r])
-    mm = [tuple(int(v) for v in t.tolist()) for t in comm.allgather(ops.toa_range(hits, n))]
-    for s in range(G):
-        for t in range(s + 2, G):
-            if mm[t][0] <= mm[s][1] + dt_max:
-                raise ShardError(f"an edge could skip a rank ({s} -> {t}): blocks too small for dt_max")
-    # 2. halo for rank r-1, exchange with neighbours
-    if r > 0:
-        halo_send, idx_send, c_send = ops.select_halo(hits, n, mm[r - 1][1] + dt_max)
-    else:
-        halo_send, idx_send, c_send = ops.empty_hits(0), ops.empty_u32(0), 0
-    counts = [int(t[0].item()) for t in comm.allgather(ops.scalar_tensor([c_send]))]
-    c_recv = counts[r + 1] if r + 1 < G else 0
-    halo_recv, idx_recv = ops.empty_hits(c_recv), ops.empty_u32(c_recv)
-    comm.exchange(r - 1 if r > 0 and c_send else None, [halo_send, idx_send],
-                  r + 1 if c_recv else None, [halo_recv, idx_recv])
-    # 3. cluster [owned | halo], features from owned hits only
-    X = ops.cat(hits, halo_recv) if c_recv else hits
-    labels, feats, k = ops.cluster_partial(X, n + c_recv, n)
-    ops.translate(labels, n + c_recv, n, o_r, idx_recv, int(offs[r + 1]) if r + 1 < G else 0)
-    ops.offset_feature_labels(feats, k, o_r)
-    # 4. boundary pairs: my label vs the next rank's label of each halo hit
-    lab_send = ops.gather(labels, idx_send, c_send) if c_send else ops.empty_u32(0)
-    lab_peer = ops.empty_u32(c_recv)
-    comm.exchange(r - 1 if r > 0 and c_send else None, [lab_send], r + 1 if c_recv else None, [lab_peer])
-    pairs, p = ops.make_pairs(labels[n:n + c_recv], lab_peer, c_recv)
-    pcounts = [int(t[0].item()) for t in comm.allgather(ops.scalar_tensor([p]))]
-    pmax = max(pcounts)
-    all_pairs, P = None, sum(pcounts)
-    if P:
-        pad = ops.zeros_pairs(pmax)
-        pad[:p] = pairs[:p]
-        gathered = comm.allgather(pad)
-        all_pairs = ops.concat_rows([g[:c] for g, c in zip(gathered, pcounts)])
-    mp = ops.union_pairs(all_pairs, P) if P else ops.union_pairs(None, 0)
-    # 5. relabel, split records, gather partials, fold the ones this rank owns
-    ops.relabel(labels, n, mp)
-    kept, nk, part, q = ops.split(feats, k, mp)
-    qcounts = [int(t[0].item()) for t in comm.allgather(ops.scalar_tensor([q]))]
-    Q = sum(qcounts)
-    all_part = ops.empty_feats(0)
-    if Q:
-        qmax = max(qcounts)
-        padf = ops.empty_feats(qmax)
-        padf[:q] = part[:q]
-        gathered = comm.allgather(padf)
-        all_part = ops.concat_rows([g[:c] for g, c in zip(gathered, qcounts)])
-    out, k_out = ops.fold(kept, nk, all_part, Q, o_r, o_r + n, nk + Q)
-    stats = {"halo_sent": c_send, "halo_recv": c_recv, "pairs": p, "pairs_total": P, "partials": q,
-             "partials_total": Q, "local_clusters": k}
-    return ShardResult(labels[:n], out, k_out, o_r, stats)
+class ShardedClusterer:
+    """One context + workspace for ``tpx_cluster_run_sharded`` on ``comm``."""
+
+    def __init__(self, dt_max: int, comm: _Comm, width: int = 256, height: int = 256):
+        self.ctx = _tpx.Clusterer(dt_max, width, height)
+        self.comm = comm
+        self._ws = None
+
+    def workspace_bytes(self, n: int) -> int:
+        _, world = self.comm.rank_world()
+        b = ctypes.c_size_t(0)
+        _tpx._check(_tpx._sharded_ws(self.ctx._h, int(n), world, ctypes.byref(b)),
+                    "tpx_cluster_sharded_workspace_bytes")
+        return b.value
+
+    def run(self, hits, n: int | None = None, labels=None, features=None, capacity: int | None = None,
+            stream=None) -> ShardResult:
+        import torch
+
+        assert hits.is_cuda and hits.is_contiguous()
+        if n is None:
+            n = hits.numel() * hits.element_size() // HIT_BYTES
+        dev = hits.device
+        if labels is None:
+            labels = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        if capacity is None:
+            capacity = n if features is None else features.numel() * features.element_size() // FEAT_BYTES
+        if features is None:
+            features = torch.empty((max(capacity, 1), FEAT_BYTES), dtype=torch.uint8, device=dev)
+        need = self.workspace_bytes(n)
+        if self._ws is None or self._ws.numel() < need or self._ws.device != dev:
+            self._ws = None
+            self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        k, off = _tpx._u64(0), _tpx._u64(0)
+        rc = _tpx._run_sharded(self.ctx._h, self.comm.handle, hits.data_ptr(), int(n), labels.data_ptr(),
+                               features.data_ptr(), int(capacity), ctypes.byref(k), ctypes.byref(off),
+                               self._ws.data_ptr(), self._ws.numel(), _tpx._stream_handle(stream))
+        if rc != _tpx.TPX_OK:
+            raise ShardError(f"tpx_cluster_run_sharded: {_tpx.status_string(rc)} ({rc})")
+        st = self.ctx.stats()
+        return ShardResult(labels[:n], features[: min(k.value, capacity)], k.value, off.value, st)
+
+    def close(self):
+        self.ctx.close()
+        self._ws = None
+
+
+def cluster_sharded(hits, dt_max: int, comm: _Comm, width: int = 256, height: int = 256, stream=None) -> ShardResult:
+    """One sharded run of this rank's block ``hits`` (device, [n_r, 16] bytes)."""
+    c = ShardedClusterer(dt_max, comm, width, height)
+    try:
+        return c.run(hits, stream=stream)
+    finally:
+        c.close()

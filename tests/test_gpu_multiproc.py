@@ -1,8 +1,9 @@
 """GPU: the sharded path as real processes (torchrun, 2 ranks) on one B200.
 
-The gpurun pool gives one GPU, so both ranks share it and the process group
-is gloo with collectives staged through host memory (TorchComm(staged=True));
-the kernels, the halo / pair / partial-record protocol and the process-level
+The gpurun pool gives one GPU, so both ranks share it (NCCL refuses two ranks
+on one device): the process group is gloo and tpx_cluster_run_sharded uses
+the library's host-callback transport (sharded.HostComm + TorchAdapter); the
+kernels, the halo / pair / partial-record protocol and the process-level
 plumbing are the ones a multi-GPU NCCL run uses.  Rank 0 checks the
 concatenated outputs against the oracle bit for bit (tools/sharded_check.py).
 """

@@ -1,11 +1,14 @@
-"""Multi-rank protocol of the ToA-sharded path on CPU (-m "not gpu").
+"""Multi-rank ToA-sharded path on CPU (-m "not gpu").
 
-The protocol code is the product's (paper_2412_11809_b200/sharded.py); the
-per-rank compute steps run on the numpy/oracle backend (tests/sharded_ref.py)
-so that the exchange logic -- halo selection, halo send/recv, label pairs,
-union pass, partial folding -- is checked with real gloo process groups
-(world size 2, 127.0.0.1) and with in-process thread ranks.  Concatenated in
-rank order, the ranks' outputs must equal the single-process oracle exactly.
+1. The protocol scheme (tests/sharded_ref.py: a numpy/oracle model of the
+   exchange steps the library runs in csrc/sharded.cuh -- halo selection,
+   halo send/recv, label pairs, union pass, partial folding) with real gloo
+   process groups (world size 2, 127.0.0.1) and in-process thread ranks:
+   concatenated in rank order, the ranks' outputs equal the oracle exactly.
+2. The library's host-callback transport (tpx_comm_create_host, the
+   transport of functional multi-rank runs without NCCL) with the product
+   adapters of paper_2412_11809_b200/sharded.py -- gloo world size 2 and
+   thread ranks -- through tpx_comm_selftest (host buffers, no GPU).
 """
 import os
 import socket
@@ -18,6 +21,7 @@ import torch
 import oracle
 import tpxgen
 from paper_2412_11809_b200 import sharded
+from tests import sharded_ref as model
 from tests.sharded_ref import NumpyOps, _feats
 
 
@@ -27,15 +31,15 @@ def _blocks(n, G):
 
 
 def _run_threads(h, dt, G, W=256, H=256):
-    group = sharded.ThreadGroup(G)
+    group = model.ThreadGroup(G)
     out = [None] * G
     err = []
 
     def worker(r, lo, hi):
         try:
-            comm = sharded.ThreadComm(group, r)
+            comm = model.ThreadComm(group, r)
             t = torch.from_numpy(h[lo:hi].view(np.uint8).reshape(-1, 16).copy())
-            out[r] = sharded.cluster_sharded(t, dt, comm, NumpyOps(dt, W, H))
+            out[r] = model.model_cluster_sharded(t, dt, comm, NumpyOps(dt, W, H))
         except Exception as e:  # pragma: no cover - surfaced below
             err.append(e)
             group.barrier.abort()
@@ -78,7 +82,7 @@ def test_cluster_spanning_three_ranks():
 
 def test_rank_skipping_edge_is_rejected():
     h = tpxgen.generate("mixed", n_hits=3000)
-    with pytest.raises(sharded.ShardError):
+    with pytest.raises(model.ModelShardError):
         _run_threads(h, 10**9, 3)
 
 
@@ -90,7 +94,7 @@ def _gloo_worker(rank, world, port, h, dt, q):
     try:
         lo, hi = _blocks(len(h), world)[rank]
         t = torch.from_numpy(h[lo:hi].view(np.uint8).reshape(-1, 16).copy())
-        res = sharded.cluster_sharded(t, dt, sharded.TorchComm(), NumpyOps(dt))
+        res = model.model_cluster_sharded(t, dt, model.TorchComm(), NumpyOps(dt))
         q.put((rank, res.labels.numpy().copy(), res.features.numpy().copy(), res.stats))
     finally:
         dist.destroy_process_group()
@@ -125,3 +129,52 @@ def test_gloo_world_size_2_matches_oracle():
     assert np.array_equal(labels, rl)
     assert feats.tobytes() == rf.tobytes()
     assert res[0][2]["halo_recv"] > 0 and res[1][2]["halo_sent"] > 0
+
+
+# ------------------------------------------------ the library's host transport
+def test_host_transport_thread_ranks():
+    G = 3
+    group = sharded.ThreadGroup(G)
+    rcs = [None] * G
+
+    def worker(r):
+        comm = sharded.HostComm(sharded.ThreadAdapter(group, r))
+        assert comm.rank_world() == (r, G)
+        rcs[r] = comm.selftest(5000)
+        comm.close()
+
+    ths = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert rcs == [0] * G
+
+
+def _gloo_transport_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        comm = sharded.HostComm(sharded.TorchAdapter())
+        q.put((rank, comm.rank_world(), comm.selftest(70_000)))
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_transport_gloo_world_size_2():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_transport_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, (0, 2), 0), (1, (1, 2), 0)]

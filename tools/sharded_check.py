@@ -3,8 +3,8 @@
 Every rank clusters its contiguous block of a seeded mixed stream with
 sharded.cluster_sharded; rank 0 gathers the blocks' labels and records and
 compares their concatenation with the CPU oracle bit for bit.  Backend from
-TPX_DIST_BACKEND (nccl, one GPU per rank; gloo: ranks may share a GPU and the
-collectives are staged through host memory).
+TPX_DIST_BACKEND (nccl: tpx_nccl_comm_init, one GPU per rank; gloo: the
+library's host-callback transport, ranks may share a GPU).
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/sharded_check.py [n_hits] [preset]
 """
 import os
@@ -35,8 +35,10 @@ def main():
     cuts = np.linspace(0, n, world + 1).astype(np.int64)
     lo, hi = int(cuts[rank]), int(cuts[rank + 1])
     x = torch.from_numpy(h[lo:hi].view(np.uint8).reshape(-1, 16).copy()).to(dev)
-    comm = sharded.TorchComm(staged=(backend != "nccl"))
-    res = sharded.cluster_sharded(x, dt, comm, sharded.CudaOps(dt))
+    # NCCL: library-owned communicator (one GPU per rank); gloo: the library's
+    # host-callback transport over the process group (ranks may share a GPU)
+    comm = sharded.NcclComm() if backend == "nccl" else sharded.HostComm(sharded.TorchAdapter())
+    res = sharded.cluster_sharded(x, dt, comm)
     torch.cuda.synchronize()
     mine = (res.labels.cpu().numpy().view(np.uint32).copy(),
             res.features.cpu().numpy().reshape(-1).view(oracle.FEAT_DTYPE).copy())
