@@ -148,6 +148,22 @@ def cpu_baseline(h_sample, dt, label: str):
     return rec, ref
 
 
+def _cpu_parallel(sample, dt, rl, rf, ns):
+    import cpu_parallel
+
+    cores = len(os.sched_getaffinity(0))
+    cpu_parallel.cluster(sample[: min(len(sample), 200_000)], dt, threads=cores)  # warm-up (page-in, threads)
+    t0 = time.perf_counter()
+    gl, gf, st = cpu_parallel.cluster(sample, dt, threads=cores, stats=True)
+    t = time.perf_counter() - t0
+    same = bool(np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes())
+    return {"value": round(ns / t / 1e6, 2), "unit": "Mhit/s", "cores": cores, "seconds": round(t, 3),
+            "kind": "parallel CPU comparator: temporal splitting into 100*dt_max windows, Alg. 1 per window, "
+                    "merge cascade for border clusters (PAPER.md §3.2.3, §3.3)",
+            "sample": f"first {ns} hits of the same {PRESET} stream", "parity_vs_oracle": "bit-exact" if same else "MISMATCH",
+            "border_clusters": int(st["border_clusters"]), "merges": int(st["merges"]), "cpu_model": _cpu_model()}
+
+
 def run_reference(args):
     """Reference arm: the CPU oracle, on the box's host cores (1 thread)."""
     ws, rank, _ = _dist()
@@ -451,6 +467,7 @@ def run_ours(args):
     # and the parity gate: the GPU path on the same prefix through the same
     # context, memcmp of labels and 64-B records against the oracle's output
     cpu = None
+    cpu_par = None
     parity = {"status": "not checked", "full_invariants": full_inv}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         ns = min(args.ref_sample, n)
@@ -462,6 +479,10 @@ def run_ours(args):
         same_f = bool(sk == len(rf) and tpx.features_to_numpy(sf).tobytes() == rf.tobytes())
         del d_s, sl, sf
         ok = same_l and same_f and full_inv
+        # the paper's parallel multi-core CPU method (cpu_parallel/, SURVEY
+        # §8(f) f4: temporal splitting + merge cascade) on the same prefix,
+        # all host cores, checked against the oracle's output
+        cpu_par = _cpu_parallel(sample, dt, rl, rf, ns)
         parity = {"status": "bit-exact" if ok else "MISMATCH", "prefix_hits": ns,
                   "prefix_labels_memcmp": same_l, "prefix_records_memcmp": same_f, "full_invariants": full_inv,
                   "full_size_memcmp": "tests/test_gpu_fullsize.py (configs[2] 200M, configs[3] 50M, configs[4] 250M shard)"}
@@ -490,6 +511,7 @@ def run_ours(args):
         "hbm_frac_whole_path": round(whole_path_gbs / peak, 4),
         "stage_ms": {k_: round(v, 4) for k_, v in stage_avg.items()},
         "cpu_baseline": cpu,
+        "cpu_parallel": cpu_par,
         "parity": parity,
         "clocks": clocks,
         "gen_seconds": round(gen_s, 2),
