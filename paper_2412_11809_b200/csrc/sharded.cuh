@@ -27,6 +27,8 @@
 //   allgather           partials of every rank (+ error flags)
 //   k_shard_fold        partials folded into the owner's records -> sync 3
 #pragma once
+#include <memory>
+
 #include "comm.h"
 
 namespace tpx {
@@ -472,6 +474,8 @@ int tpx_cluster_run_sharded(tpx_cluster* c, tpx_comm* comm, const tpx_hit* local
   const uint64_t n = n_local, dt = c->dt;
 
   // ---- 1. ranges, lent hits, counts
+  nvtx_range nv_all("tpx:sharded_run");
+  std::unique_ptr<nvtx_range> nv(new nvtx_range("tpx:shard_exchange"));
   k_shard_init<<<1, 32, 0, s>>>(st, n, reinterpret_cast<unsigned long long*>(pairs));
   TPX_LAUNCHED(c);
   const uint32_t ntiles = n_tiles_of(n, kShardTile);
@@ -511,6 +515,7 @@ int tpx_cluster_run_sharded(tpx_cluster* c, tpx_comm* comm, const tpx_hit* local
   TPX_SH(comm_sendrecv(comm, R - 1, send_idx, c_send * 4, R + 1, recv_idx, c_recv * 4, s));
   TPX_SH(comm_group_end(comm));
 
+  nv.reset();
   // ---- 2. cluster [owned | halo]: sort (sync 2) + tiles + border merge
   run_ptrs r;
   r.L = make_layout(n + c_recv);
@@ -530,6 +535,7 @@ int tpx_cluster_run_sharded(tpx_cluster* c, tpx_comm* comm, const tpx_hit* local
   TPX_SH(run_core(c, r));
 
   // ---- 3. boundary pairs of every rank, union
+  nv.reset(new nvtx_range("tpx:shard_union"));
   if (c_send) {
     k_shard_gather_labels<<<grid_for(c_send, 256), 256, 0, s>>>(labels_out, send_idx, c_send, lent_labels);
     TPX_LAUNCHED(c);
@@ -569,6 +575,7 @@ int tpx_cluster_run_sharded(tpx_cluster* c, tpx_comm* comm, const tpx_hit* local
     }
   }
 
+  nv.reset();
   // ---- 4. records: emission (merged-away records -> partials), owner fold
   unsigned long long* n_removed = &st->n_removed;
   TPX_SH(emit_sorted(c, r, part + 1, n_removed));

@@ -11,6 +11,8 @@
 // Fallbacks (taken only when the fast path reports it cannot be exact):
 //   wider sort window -> global LSD radix sort (sort.cuh) -> global
 //   union-find pipeline (cluster.cuh).
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -27,6 +29,15 @@
 #include "tile_cc.cuh"
 
 using namespace tpx;
+
+// NVTX range over a stage's launches (host timeline; header-only NVTX v3,
+// a no-op unless a profiler is attached).
+struct nvtx_range {
+  explicit nvtx_range(const char* name) { nvtxRangePushA(name); }
+  ~nvtx_range() { nvtxRangePop(); }
+  nvtx_range(const nvtx_range&) = delete;
+  nvtx_range& operator=(const nvtx_range&) = delete;
+};
 
 namespace {
 
@@ -286,6 +297,7 @@ static int readback_sync(tpx_cluster* c, void* dst, const void* dev, size_t byte
 // Global LSD radix sort into S (fallback when the windowed sort cannot prove
 // its displacement bound).  Needs the ToA range first: one extra host sync.
 static int sort_global(tpx_cluster* c, const run_ptrs& r) {
+  nvtx_range nv("tpx:sort_radix");
   dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
   const int g = grid_for(r.n, kMMThreads) < 148 * 8 ? grid_for(r.n, kMMThreads) : 148 * 8;
   k_validate_minmax<<<g, kMMThreads, 0, r.s>>>(r.hits, r.n, c->width, c->height, hdr);
@@ -311,6 +323,7 @@ static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* 
 
 // Tile clustering + border merge + ordered emission on a sorted S.
 static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
+  nvtx_range nv("tpx:tile+border_merge");
   char* ws = r.ws;
   const layout& L = r.L;
   dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
@@ -386,6 +399,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
 // the boundary merge are appended there (global labels) instead.
 static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* removed_out,
                        unsigned long long* n_removed) {
+  nvtx_range nv("tpx:emit");
   char* ws = r.ws;
   const layout& L = r.L;
   dev_hdr* hdr = (dev_hdr*)(ws + L.hdr);
@@ -743,7 +757,10 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
     c->runs_at_start = 0;
   }
   const int first_attempt = c->sort_start;
+  nvtx_range nv_run("tpx:run");
   for (int attempt = first_attempt; attempt <= kRadixAttempt + 1; ++attempt) {
+    nvtx_range nv_sort(attempt == 0 ? "tpx:sort_window" : attempt == 1 ? "tpx:sort_window_d2560"
+                                                       : attempt == 2 ? "tpx:sort_window_d3072" : "tpx:sort_fallback");
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {

@@ -169,3 +169,51 @@ def is_refinement(fine, coarse) -> bool:
         if m.setdefault(a, b) != b:
             return False
     return True
+
+
+def streaming_last_writer(h, dt: int, variant: int) -> np.ndarray:
+    """Variants (iii)(b) GLOBAL (variant 1) / (iii)(c) STATIC (variant 2) with
+    SPEC's per-pixel reference matrix ("PixelRefMatrix"): hits in
+    (toa, index) order; for each of the 9 pixels only the cluster of the
+    pixel's LAST hit is a candidate; it is joinable if toa - maxToA (b) /
+    toa - minToA (c) <= dt; the hit joins and merges every joinable
+    candidate.  Structurally different from the oracle (reading R21: every
+    cluster with any member on the 9 pixels).  The two readings coincide:
+    a hit on pixel p that did not join cluster A (which has a member on p)
+    found A non-joinable, and A can never become joinable again (maxToA /
+    minToA only change when a hit joins), so an overwritten reference only
+    ever hides a dead cluster."""
+    n = len(h)
+    order = np.lexsort((np.arange(n), h["toa"].astype(np.int64)))
+    parent = list(range(n))
+    cmin, cmax, cidx = {}, {}, {}
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    last = {}
+    xs, ys, ts = h["x"].tolist(), h["y"].tolist(), h["toa"].tolist()
+    for i in order.tolist():
+        xi, yi, ti = xs[i], ys[i], ts[i]
+        cands = set()
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                j = last.get((xi + dx, yi + dy))
+                if j is None:
+                    continue
+                r = find(j)
+                ref = cmax[r] if variant == 1 else cmin[r]
+                if ti - ref <= dt:
+                    cands.add(r)
+        root = i
+        cmin[i], cmax[i], cidx[i] = ti, ti, i
+        for r in cands:
+            a, b = min(root, r), max(root, r)
+            parent[b] = a
+            cmin[a], cmax[a], cidx[a] = min(cmin[a], cmin[b]), max(cmax[a], cmax[b]), min(cidx[a], cidx[b])
+            root = a
+        last[(xi, yi)] = i
+    return np.array([cidx[find(i)] for i in range(n)], dtype=np.uint32)

@@ -349,3 +349,73 @@ def test_streaming_variant_invariants():
             assert (np.diff(t) <= dt).all()
         for lab_arr in (lb, lc):  # canonical labels
             assert (lab_arr <= np.arange(len(h))).all() and np.array_equal(lab_arr[lab_arr], lab_arr)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_streaming_variants_last_writer_reading(variant):
+    """Second implementation of the (b)/(c) streaming oracle (SPEC's
+    per-pixel last-writer reference matrix, pins.streaming_last_writer):
+    identical labels on fuzz inputs dense enough that pixels are re-hit and
+    clusters merge (the R21 reading and the last-writer reading)."""
+    rng = np.random.default_rng(100 + variant)
+    for _ in range(150):
+        n = int(rng.integers(1, 400))
+        W, H = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        dt = int(rng.integers(0, 200))
+        h = tpxgen.random_small(rng, n, W, H, int(rng.integers(0, 10 * (dt + 1))))
+        got = oracle.cluster_streaming(h, dt, variant, W, H)
+        want = pins.streaming_last_writer(h, dt, variant)
+        assert np.array_equal(got, want), (variant, n, W, H, dt)
+    for preset in ("tiny", "heavyion"):
+        h = tpxgen.generate(preset, n_hits=3000)
+        dt = tpxgen.PRESETS[preset]["dt_max"]
+        assert np.array_equal(oracle.cluster_streaming(h, dt, variant), pins.streaming_last_writer(h, dt, variant))
+
+
+def test_generator_truth_on_separated_clusters():
+    """Pin P7: where the generator's clusters are
+    separated from every other cluster (>= 2 dt_max apart in time, or bounding
+    boxes >= 2 px apart) and away from the sensor edge, the oracle's component
+    of each is exactly the generator's cluster (dots: 8-connected growth,
+    tracks: rasterised segments, all within dt_max in time)."""
+    dt = 320
+    h, truth = tpxgen.generate("mixed", n_hits=200_000, truth=True, rate_hz=20_000, seed=31)
+    labels, _ = oracle.cluster(h, dt)
+    tid = truth.astype(np.int64)
+    ids, inv = np.unique(tid, return_inverse=True)
+    k = len(ids)
+    t = h["toa"].astype(np.int64)
+    x, y = h["x"].astype(np.int64), h["y"].astype(np.int64)
+    big = np.iinfo(np.int64).max
+    tmin = np.full(k, big); np.minimum.at(tmin, inv, t)
+    tmax = np.full(k, -1); np.maximum.at(tmax, inv, t)
+    x0 = np.full(k, big); np.minimum.at(x0, inv, x)
+    x1 = np.full(k, -1); np.maximum.at(x1, inv, x)
+    y0 = np.full(k, big); np.minimum.at(y0, inv, y)
+    y1 = np.full(k, -1); np.maximum.at(y1, inv, y)
+    order = np.argsort(tmin, kind="stable")
+    sep = np.ones(k, dtype=bool)
+    for a_i, a in enumerate(order.tolist()):
+        # every earlier-starting cluster still within 2 dt in time must be >= 2 px away
+        for b in order[max(0, a_i - 50):a_i].tolist():
+            if tmax[b] + 2 * dt > tmin[a]:
+                near = not (x0[a] > x1[b] + 1 or x0[b] > x1[a] + 1 or y0[a] > y1[b] + 1 or y0[b] > y1[a] + 1)
+                if near:
+                    sep[a] = sep[b] = False
+    # clusters touching the sensor edge may have lost off-sensor pixels (the
+    # generator drops them, DESIGN §5) and so need not be connected
+    sep &= (x0 > 0) & (y0 > 0) & (x1 < 255) & (y1 < 255)
+    # the stream stops at exactly n hits in readout order: clusters within the
+    # readout disorder (<= 22.8k ticks, DESIGN §5) of the end may be truncated
+    sep &= tmin < t.max() - 50_000
+    assert sep.mean() > 0.9
+    # per separated truth cluster: one oracle label, and that label's component is exactly the cluster
+    members = {}
+    for i, c in enumerate(inv.tolist()):
+        if sep[c]:
+            members.setdefault(c, []).append(i)
+    lab_count = np.bincount(labels.astype(np.int64), minlength=len(h))
+    for c, mem in members.items():
+        ls = set(labels[mem].tolist())
+        assert len(ls) == 1, f"truth cluster {ids[c]} split: {ls}"
+        assert lab_count[ls.pop()] == len(mem), f"truth cluster {ids[c]} merged with other hits"
