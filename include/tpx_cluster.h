@@ -249,12 +249,14 @@ int tpx_cluster_last_stats(const tpx_cluster* ctx, tpx_run_stats* out);
 int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
 
 /* Tile configuration of the clustering kernel: TPX_TILE_AUTO (default) lets
- * a window-density probe on the sorted stream choose; TPX_TILE_SPARSE (2x2-pixel
- * cell index, 2048-hit tiles) / TPX_TILE_DENSE (pixel hash, large halo) force
- * one; TPX_TILE_COLUMN forces the earlier column-bucket sparse kernel (kept for
- * comparison).  Results are identical; only speed differs -- the parity tests
- * cover every mode.  Errors: INVALID_ARG. */
-enum { TPX_TILE_AUTO = 0, TPX_TILE_SPARSE = 1, TPX_TILE_DENSE = 2, TPX_TILE_COLUMN = 3 };
+ * a window-density probe on the sorted stream choose; TPX_TILE_SPARSE (2048-hit
+ * tiles, counting-sorted 2x2-pixel cell index with backward hooking for
+ * sensors up to 1024 x 1024, else the linked-list cell index) /
+ * TPX_TILE_DENSE (pixel hash, large halo) force one; TPX_TILE_COLUMN forces
+ * the earlier column-bucket sparse kernel and TPX_TILE_CELL the linked-list
+ * cell kernel (both kept for comparison).  Results are identical; only speed
+ * differs -- the parity tests cover every mode.  Errors: INVALID_ARG. */
+enum { TPX_TILE_AUTO = 0, TPX_TILE_SPARSE = 1, TPX_TILE_DENSE = 2, TPX_TILE_COLUMN = 3, TPX_TILE_CELL = 4 };
 int tpx_cluster_set_tile_mode(tpx_cluster* ctx, int mode);
 
 /* Static name of stage i (0 <= i < 16) as reported in stage_ms; "" if unused. */

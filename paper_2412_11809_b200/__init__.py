@@ -70,7 +70,7 @@ _centroids = _proto("tpx_cluster_centroids", _int, _vp, _u64, _vp, _vp)
 _last_stats = _proto("tpx_cluster_last_stats", _int, _vp, ctypes.POINTER(RunStats))
 _set_profiling = _proto("tpx_cluster_set_profiling", _int, _vp, _int)
 _set_tile_mode = _proto("tpx_cluster_set_tile_mode", _int, _vp, _int)
-TILE_MODES = {"auto": 0, "sparse": 1, "dense": 2, "column": 3}
+TILE_MODES = {"auto": 0, "sparse": 1, "dense": 2, "column": 3, "cell": 4}
 _stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
 _run_partial = _proto("tpx_cluster_run_partial", _int, _vp, _vp, _u64, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
                       _vp, ctypes.c_size_t, _vp)

@@ -18,13 +18,21 @@ constexpr int kListGrid = TPX_LIST_GRID;
 
 __device__ __forceinline__ void flag_internal(dev_hdr* hdr) { atomicOr(&hdr->err, 2u); }
 
+// Open bitmap over sorted positions (bit p = hit p belongs to an open
+// component), one word per warp and output round of the tile kernels.  Edges
+// of the global pass must join open hits only; a closed endpoint means the
+// tile path was inconsistent (checked, never expected).
+__device__ __forceinline__ bool is_open(const uint32_t* openbm, uint64_t p) {
+  return (__ldcg(openbm + (p >> 5)) >> (p & 31)) & 1u;
+}
+
 // Hits whose forward window left the staged halo: scan the rest of the window
 // (from the first position the tile did not stage) in global memory, one warp
 // per hit (lane = candidate, 32 per step); any j it reaches belongs to an open
 // component.
 __global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __restrict__ S, uint64_t n, uint64_t dt,
                                                                   const uint2* __restrict__ list, dev_hdr* hdr,
-                                                                  uint32_t* parent_g) {
+                                                                  uint32_t* parent_g, const uint32_t* openbm) {
   const uint64_t cnt = hdr->n_overflow;
   const unsigned lane = lane_id();
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -43,7 +51,7 @@ __global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __
         adj = in && adjacent(a.xy, b.xy);
       }
       if (adj) {
-        if (ld_cg(parent_g + j) == kSentinel) flag_internal(hdr);
+        if (!is_open(openbm, j)) flag_internal(hdr);
         else uf_unite(parent_g, i, (uint32_t)j);
       }
       if (!__all_sync(kFull, in)) break;  // past the window (sorted by ToA)
@@ -85,11 +93,11 @@ __global__ void __launch_bounds__(kListThreads) k_flatten_open(const uint32_t* _
 }
 
 __global__ void __launch_bounds__(kListThreads) k_pair_unions(const uint2* __restrict__ pairs, dev_hdr* hdr,
-                                                              uint32_t* parent_g) {
+                                                              uint32_t* parent_g, const uint32_t* openbm) {
   const uint64_t cnt = hdr->n_pairs;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 p = pairs[t];
-    if (ld_cg(parent_g + p.x) == kSentinel || ld_cg(parent_g + p.y) == kSentinel) {
+    if (!is_open(openbm, p.x) || !is_open(openbm, p.y)) {
       flag_internal(hdr);
       return;
     }

@@ -103,6 +103,7 @@ struct tile_args {
   uint32_t n_owned;          // hits with input index >= n_owned carry no features (sharded halo)
   uint32_t* labels;          // labels_out (input order)
   uint32_t* parent_g;        // global union-find over sorted positions (open hits only)
+  uint32_t* openbm;          // open bitmap over sorted positions (finalize.cuh is_open)
   uint32_t* slot_of;         // root position -> stage slot (open components)
   tpx_cluster_features* stage;  // [n_tiles * kTile]
   uint32_t* comp_count;      // [n_tiles]
@@ -494,6 +495,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       const uint32_t oh = warp_append(v, &a.hdr->n_open_hits);
       const uint32_t oc = warp_append(v, &a.hdr->n_open_comps);
       const uint32_t ov = warp_append(v, &a.hdr->n_overflow);
+      {
+        const unsigned om = __ballot_sync(kFull, v);  // every hit is open
+        if (lane_id() == 0) a.openbm[(t0 + j) >> 5] = om;
+      }
       if (v) {
         const uint64_t pos = t0 + j;
         const bool own = r.idx < a.n_owned;
@@ -971,6 +976,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       }
       else a.slot_of[pos] = (uint32_t)(t0 + crank[j]);
     }
+    {  // open word of these 32 positions (lane 0's position is 32-aligned; zeroed before the kernel)
+      const unsigned om = __ballot_sync(kFull, v && open);
+      if (lane_id() == 0 && om) a.openbm[pos >> 5] = om;
+    }
     const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);
     if (is_root && open) a.open_comps[oc] = (uint32_t)pos;
     const uint32_t oh = warp_append(v && open, &a.hdr->n_open_hits);
@@ -981,7 +990,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         a.parent_g[pos] = (uint32_t)(t0 + r);
         a.open_hits[oh] = (uint32_t)pos;
       } else {
-        a.parent_g[pos] = kSentinel;
         store_label(a.labels, a.n_owned, a.lm, rq[q].idx, label);
       }
       if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile

@@ -137,6 +137,10 @@ __device__ __forceinline__ void tile_run_wide(const tile_args& a, uint64_t t0, u
     const uint32_t oh = warp_append(v, &a.hdr->n_open_hits);
     const uint32_t oc = warp_append(v, &a.hdr->n_open_comps);
     const uint32_t ov = warp_append(v, &a.hdr->n_overflow);
+    {
+      const unsigned om = __ballot_sync(kFull, v);  // every hit is open
+      if (lane_id() == 0) a.openbm[(t0 + j) >> 5] = om;
+    }
     if (v) {
       const uint64_t pos = t0 + j;
       const bool own = r.idx < a.n_owned;
@@ -630,6 +634,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
     }
     const bool ovf = v && (hflag[j] & 2u);
     if (__ballot_sync(kFull, (v && open) || ovf)) {  // warp-uniform: most warps have no open hit
+      const unsigned om = __ballot_sync(kFull, v && open);  // open word (zeroed before the kernel)
+      if (lane_id() == 0 && om) a.openbm[pos >> 5] = om;  // lane 0's position is 32-aligned
       const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);
       if (is_root && open) a.open_comps[oc] = (uint32_t)pos;
       const uint32_t oh = warp_append(v && open, &a.hdr->n_open_hits);
@@ -641,7 +647,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
       if (open) {
         a.parent_g[pos] = (uint32_t)(t0 + r);
       } else {
-        a.parent_g[pos] = kSentinel;
         store_label(a.labels, a.n_owned, a.lm, tidx[q], label);
       }
     }

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "finalize.cuh"
 #include "tile_cell.cuh"
+#include "tile_csr.cuh"
 #include "group.cuh"
 #include "variant.cuh"
 #include "scan.cuh"
@@ -49,7 +50,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 uint32_t n_tiles_of(uint64_t n, int tile) { return (uint32_t)((n + tile - 1) / tile); }
 
 struct layout {
-  size_t hdr, probe, S, parent, slot_of, stage, comp_count, tmeta, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
+  size_t hdr, probe, S, parent, openbm, slot_of, stage, comp_count, tmeta, open_hits, open_comps, overflow, pairs, bitmap, wcnt, partials;
   size_t keys0, keys1, vals0, vals1, hist, minidx, flags, ord;
   size_t total;
   uint32_t tiles, nwords;
@@ -72,6 +73,7 @@ layout make_layout(uint64_t n) {
   L.probe = take(kProbeSamples * 4);
   L.S = take(n * 16);
   L.parent = take(n * 4);
+  L.openbm = take((size_t)n_tiles_of(n, kMaxTile) * kMaxTile / 8);  // one bit per position of every tile
   L.slot_of = take(n * 4);
   L.stage = take((size_t)n_tiles_of(n, kMaxTile) * kMaxTile * 64);
   L.comp_count = take((size_t)L.tiles * 4);
@@ -155,6 +157,8 @@ static int ensure_cuda(tpx_cluster* c) {
                            (int)window_sort_smem<20>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_window_sort<20, kSortTm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_smem<20>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tile_csr<csr_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)csr_smem_bytes<csr_sparse>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_dense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -254,6 +258,7 @@ struct run_ptrs {
   bool dense;   // tile configuration chosen by the density probe
   uint32_t sort_T = kWSortTile;  // output tile of the sort that produced S (its borders are verified)
   bool column;  // legacy column-bucket sparse kernel (TPX_TILE_COLUMN, comparison only)
+  bool csr = false;  // counting-sorted cell index + backward hooking (tile_csr.cuh)
   // sharded runs (sharded.cuh): labels written as global indices into two
   // arrays, emission deferred until the boundary clusters are merged
   label_map lm = {};
@@ -274,6 +279,8 @@ static int reset_header(tpx_cluster* c, const run_ptrs& r) {
   k_reset_hdr<<<1, 32, 0, r.s>>>((dev_hdr*)(r.ws + r.L.hdr));
   TPX_LAUNCHED(c);
   TPX_CUDA(cudaMemsetAsync(r.ws + r.L.bitmap, 0, (size_t)r.L.nwords * 4, r.s));
+  // open bitmap: tile kernels store only the words that have an open hit
+  TPX_CUDA(cudaMemsetAsync(r.ws + r.L.openbm, 0, (size_t)n_tiles_of(r.n, kMaxTile) * kMaxTile / 8, r.s));
   return TPX_OK;
 }
 
@@ -348,6 +355,7 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.n_owned = (uint32_t)r.n_owned;
   a.labels = r.labels;
   a.parent_g = parent_g;
+  a.openbm = (uint32_t*)(ws + L.openbm);
   a.slot_of = slot_of;
   a.stage = stage;
   a.comp_count = comp_count;
@@ -368,7 +376,15 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   else if (r.column)
     k_tile_cc<tile_sparse><<<n_tiles_of(r.n, tile_sparse::kTile), tile_sparse::kThreads,
                              tile_smem_bytes<tile_sparse>(), r.s>>>(a);
-  else {
+  else if (r.csr) {
+    static_assert(csr_sparse::kTile == cell_sparse::kTile && csr_sparse::kHalo == cell_sparse::kHalo, "shared bounds");
+    const uint32_t nt = n_tiles_of(r.n, csr_sparse::kTile);
+    a.tile_meta = (const uint64_t*)(ws + L.tmeta);
+    k_tile_bounds<cell_sparse><<<(nt + 7) / 8, 256, 0, r.s>>>(S, r.n, c->dt, nt, r.sort_T, (uint64_t*)(ws + L.tmeta),
+                                                             hdr);
+    TPX_LAUNCHED(c);
+    k_tile_csr<csr_sparse><<<nt, csr_sparse::kThreads, csr_smem_bytes<csr_sparse>(), r.s>>>(a);
+  } else {
     const uint32_t nt = n_tiles_of(r.n, cell_sparse::kTile);
     a.tile_meta = (const uint64_t*)(ws + L.tmeta);
     k_tile_bounds<cell_sparse><<<(nt + 7) / 8, 256, 0, r.s>>>(S, r.n, c->dt, nt, r.sort_T, (uint64_t*)(ws + L.tmeta),
@@ -379,9 +395,9 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   TPX_LAUNCHED(c);
 
   if (c->profiling) cudaEventRecord(c->ev[2], r.s);
-  k_overflow_unions<<<kListGrid, kListThreads, 0, r.s>>>(S, r.n, c->dt, overflow, hdr, parent_g);
+  k_overflow_unions<<<kListGrid, kListThreads, 0, r.s>>>(S, r.n, c->dt, overflow, hdr, parent_g, a.openbm);
   TPX_LAUNCHED(c);
-  k_pair_unions<<<kListGrid, kListThreads, 0, r.s>>>(pairs, hdr, parent_g);
+  k_pair_unions<<<kListGrid, kListThreads, 0, r.s>>>(pairs, hdr, parent_g, a.openbm);
   TPX_LAUNCHED(c);
   k_flatten_open<<<kListGrid, kListThreads, 0, r.s>>>(open_hits, hdr, parent_g);
   TPX_LAUNCHED(c);
@@ -676,7 +692,7 @@ int tpx_cluster_set_profiling(tpx_cluster* c, int enable) {
 }
 
 int tpx_cluster_set_tile_mode(tpx_cluster* c, int mode) {
-  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_COLUMN) return TPX_ERR_INVALID_ARG;
+  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_CELL) return TPX_ERR_INVALID_ARG;
   c->tile_mode = mode;
   return TPX_OK;
 }
@@ -827,6 +843,8 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
         r.dense = c->tile_mode == TPX_TILE_DENSE;
       }
       r.column = c->tile_mode == TPX_TILE_COLUMN;
+      r.csr = !r.dense && !r.column && c->tile_mode != TPX_TILE_CELL && c->width <= kCsrMaxCoord + 1 &&
+              c->height <= kCsrMaxCoord + 1;
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
     c->stats.sort_retries = (attempt < kRadixAttempt ? attempt : kRadixAttempt) -
