@@ -34,9 +34,9 @@ constexpr int kSortT0 = 8192;
 constexpr int kSortTm = 5120;
 constexpr int kSortT1 = 4096;
 
-template <int IT, int T = kWSortTile>
+template <int IT, int T = kWSortTile, int NT = kWSortThreads>
 struct wsort_cfg {
-  static constexpr int W = kWSortThreads * IT;         // window capacity
+  static constexpr int W = NT * IT;                    // window capacity
   static constexpr int kT = T;                         // output records per CTA
   static constexpr int D = (W - T) / 2;                // displacement bound
   static constexpr int PER_WARP = IT * 32;
@@ -76,11 +76,13 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
   return r;
 }
 
-template <int IT, int T>
-__global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, uint64_t n,
+template <int IT, int T, int NT = kWSortThreads>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort(hit_src hits, uint64_t n,
                                                                    uint32_t width, uint32_t height,
                                                                    srec* __restrict__ out, dev_hdr* hdr) {
-  using C = wsort_cfg<IT, T>;
+  using C = wsort_cfg<IT, T, NT>;
+  constexpr int kWarps = NT / 32;
+  static_assert(kWRadix <= NT, "one scan thread per digit");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);                       // [W]
   uint16_t* sval = reinterpret_cast<uint16_t*>(skey + C::W);                     // [W]
@@ -93,41 +95,47 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, 
   const uint32_t m = (uint32_t)(we - ws);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
 
-  // ---- load the window (warp-blocked: warp w owns positions [w*PER_WARP, ...))
-  uint64_t toa[IT];
-  unsigned long long mn = ~0ull, mx = 0;
-  unsigned bad = 0;
+  // ---- load the window (warp-blocked: warp w owns positions [w*PER_WARP, ...)).
+  // Keys are kept as 32-bit offsets from a provisional origin (the window's
+  // first ToA - 2^31), so no 64-bit ToA array lives in registers; a ToA more
+  // than 2^31 ticks from the first one (only possible if the window spans
+  // >= 2^31 ticks) sends the window to the fallback like a >= 2^32 span.
+  const uint64_t org = (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(hits + ws)) - 0x80000000ull;
+  uint32_t key[IT];
+  uint32_t mn = 0xffffffffu, mx = 0;
+  unsigned bad = 0, far = 0;
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
-    toa[r] = 0;
+    key[r] = 0;
     if (p < m) {
       hit4 h = load_hit(hits + (ws + p));
-      toa[r] = h.toa;
-      mn = min(mn, (unsigned long long)h.toa);
-      mx = max(mx, (unsigned long long)h.toa);
+      const uint64_t d = h.toa - org;
+      far |= (d >> 32) != 0;
+      key[r] = (uint32_t)d;
+      mn = min(mn, key[r]);
+      mx = max(mx, key[r]);
       bad |= (h.x >= width) | (h.y >= height) | (h.toa >> 48 != 0);
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->err, 1u);
-  const unsigned long long base = block_min_u64(mn, red);
-  const unsigned long long top = block_max_u64(mx, red);
-  const unsigned long long range = top - base;
-  if (range >> 32) {  // window wider than 32 bits of ticks: leave it to the fallback
+  const uint32_t kmin = (uint32_t)block_min_u64(mn, red);
+  const uint32_t kmax = (uint32_t)block_max_u64(mx, red);
+  if (__syncthreads_or(far)) {  // window wider than 2^31 ticks: leave it to the fallback
     if (threadIdx.x == 0) {
       atomicAdd(&hdr->sort_bad, 1u);
       atomicOr(&hdr->err, 4u);  // a wider displacement bound cannot help: radix for this run only
     }
     return;
   }
-  const int bits = range ? 64 - __clzll(range) : 0;
+  const uint32_t range = kmax - kmin;
+  const int bits = range ? 32 - __clz(range) : 0;
   const int passes = (bits + kWDigitBits - 1) / kWDigitBits;
-  uint32_t key[IT];
   uint32_t vl[IT];  // low 16 bits: window position (payload); high 16: rank within the warp
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
-    key[r] = (uint32_t)(toa[r] - base);
+    key[r] -= kmin;
     vl[r] = p;
   }
 
@@ -135,10 +143,10 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, 
   // cnt is warp-major (cnt[w * kWRadix + d]): lanes of a warp touch banks d % 32,
   // so counter traffic is (nearly) conflict-free; equal digits are grouped by
   // __match_any_sync and only the group leader writes.
-  __shared__ uint32_t dsum[kWSortThreads / 32];
+  __shared__ uint32_t dsum[NT / 32];
   for (int pass = 0; pass < passes || pass == 0; ++pass) {
     const int shift = pass * kWDigitBits;
-    for (int i = threadIdx.x; i < kWRadix * kWSortWarps; i += kWSortThreads) cnt[i] = 0;
+    for (int i = threadIdx.x; i < kWRadix * kWarps; i += NT) cnt[i] = 0;
     __syncthreads();
     uint32_t* wc = cnt + warp * kWRadix;
 #pragma unroll
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, 
       uint32_t tot = 0;
       if (threadIdx.x < kWRadix) {
 #pragma unroll
-        for (int w = 0; w < kWSortWarps; ++w) tot += cnt[w * kWRadix + threadIdx.x];
+        for (int w = 0; w < kWarps; ++w) tot += cnt[w * kWRadix + threadIdx.x];
       }
       uint32_t x = tot;  // inclusive scan of digit totals over threads 0..kWRadix-1
 #pragma unroll
@@ -174,7 +182,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, 
         uint32_t basev = x - tot;
         for (unsigned w2 = 0; w2 < warp; ++w2) basev += dsum[w2];
 #pragma unroll
-        for (int w = 0; w < kWSortWarps; ++w) {
+        for (int w = 0; w < kWarps; ++w) {
           const uint32_t c = cnt[w * kWRadix + threadIdx.x];
           cnt[w * kWRadix + threadIdx.x] = basev;
           basev += c;
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, 
   // ---- write the middle T records (window-local ranks [k0-ws, k0-ws+T))
   const uint32_t ofs = (uint32_t)(k0 - ws);
   const uint32_t cnt_out = (uint32_t)min((uint64_t)T, n - k0);
-  for (uint32_t j = threadIdx.x; j < cnt_out; j += kWSortThreads) {
+  for (uint32_t j = threadIdx.x; j < cnt_out; j += NT) {
     const uint64_t gi = ws + sval[ofs + j];
     hit4 h = load_hit(hits + gi);
     srec r;
@@ -220,9 +228,9 @@ __global__ void __launch_bounds__(kWSortThreads, 2) k_window_sort(hit_src hits, 
   }
 }
 
-template <int IT>
+template <int IT, int NT = kWSortThreads>
 constexpr size_t window_sort_smem() {
-  return (size_t)wsort_cfg<IT>::W * 6 + (size_t)kWRadix * kWSortWarps * 4;
+  return (size_t)wsort_cfg<IT, kWSortTile, NT>::W * 6 + (size_t)kWRadix * (NT / 32) * 4;
 }
 
 // Verification of a windowed sort right after it (before any clustering

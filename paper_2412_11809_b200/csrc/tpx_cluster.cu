@@ -14,6 +14,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -27,6 +28,7 @@
 #include "scan.cuh"
 #include "sort.cuh"
 #include "sort_window.cuh"
+#include "radix_onesweep.cuh"
 #include "tile_cc.cuh"
 
 using namespace tpx;
@@ -90,7 +92,10 @@ layout make_layout(uint64_t n) {
   L.keys1 = take(n * 8);
   L.vals0 = take(n * 4);
   L.vals1 = take(n * 4);
-  L.hist = take((size_t)rt * kRadixBins * 4);
+  {
+    const size_t hb = (size_t)rt * kRadixBins * 4, ob = os_layout::bytes(rt);  // tile histograms / onesweep words
+    L.hist = take(hb > ob ? hb : ob);
+  }
   L.minidx = take(n * 4);
   L.flags = take(n * 4);
   L.ord = take(n * 4);
@@ -149,14 +154,8 @@ struct tpx_cluster {
 // that contexts can be created (and arguments validated) without a GPU.
 static int ensure_cuda(tpx_cluster* c) {
   if (c->cuda_ready) return TPX_OK;
-  if (cudaFuncSetAttribute(k_window_sort<20, kSortT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)window_sort_smem<20>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_window_sort_kv<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_window_sort_kv<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)window_sort_kv_smem<12>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_window_sort<20, kSortT1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)window_sort_smem<20>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_window_sort<20, kSortTm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)window_sort_smem<20>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_csr<csr_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)csr_smem_bytes<csr_sparse>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -208,6 +207,37 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
   uint32_t* hist = (uint32_t*)(ws + L.hist);
   uint32_t* partials = (uint32_t*)(ws + L.partials);
   const uint32_t tiles = n_tiles_of(n, kRadixTile);
+  if constexpr (sizeof(KeyT) == 4) {
+    // single-sweep passes (radix_onesweep.cuh): one digit-total read, then
+    // one kernel per pass
+    if (passes > 0) {
+      char* sc = (char*)hist;
+      uint32_t* gcount = (uint32_t*)(sc + os_layout::gcount);
+      uint32_t* ticket = (uint32_t*)(sc + os_layout::ticket);
+      unsigned long long* status = (unsigned long long*)(sc + os_layout::status);
+      TPX_CUDA(cudaMemsetAsync(sc, 0, os_layout::bytes(tiles), s));
+      const uint32_t hg = tiles < 148 * 8 ? tiles : 148 * 8;
+      k_os_hist<<<hg, 256, 0, s>>>(hits, n, toa_min, passes, gcount);
+      TPX_LAUNCHED(c);
+      for (int p = 0; p < passes; ++p) {
+        if (p == 0)
+          k_os_pass<true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, p, tiles, gcount, ticket,
+                                                          status, (uint32_t*)k1, v1);
+        else
+          k_os_pass<false><<<tiles, kRadixThreads, 0, s>>>(hits, (const uint32_t*)k0, v0, n, toa_min, p, tiles, gcount,
+                                                           ticket, status, (uint32_t*)k1, v1);
+        TPX_LAUNCHED(c);
+        KeyT* tk = k0;
+        k0 = k1;
+        k1 = tk;
+        uint32_t* tv = v0;
+        v0 = v1;
+        v1 = tv;
+      }
+    }
+    *perm_out = passes ? v0 : nullptr;
+    return TPX_OK;
+  }
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
     if (p == 0) {
@@ -327,6 +357,28 @@ static int sort_global(tpx_cluster* c, const run_ptrs& r) {
 
 static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* removed_out,
                        unsigned long long* n_removed);
+
+// One windowed-sort attempt (sort_window.cuh): T outputs per CTA from a
+// window of IT * NT hits (D = (IT * NT - T) / 2), then the border check.
+template <int IT, int T, int NT>
+static int window_sort(tpx_cluster* c, run_ptrs& r, srec* S, dev_hdr* hdr) {
+  static_assert(window_sort_smem<IT, NT>() <= 227 * 1024, "window sort shared memory");
+  static bool attr = false;  // once per process (the attribute is per function)
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_window_sort<IT, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)window_sort_smem<IT, NT>()) != cudaSuccess)
+      return TPX_ERR_CUDA;
+    attr = true;
+  }
+  r.sort_T = T;
+  const uint32_t sort_tiles = n_tiles_of(r.n, T);
+  k_window_sort<IT, T, NT><<<sort_tiles, NT, window_sort_smem<IT, NT>(), r.s>>>(r.hits, r.n, c->width, c->height, S,
+                                                                               hdr);
+  TPX_LAUNCHED(c);
+  k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, r.n, T, hdr);
+  TPX_LAUNCHED(c);
+  return TPX_OK;
+}
 
 // Tile clustering + border merge + ordered emission on a sorted S.
 static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
@@ -780,29 +832,11 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {
-      r.sort_T = kSortT0;
-      const uint32_t sort_tiles = n_tiles_of(n, kSortT0);
-      k_window_sort<20, kSortT0><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
-                                                                                            c->height, S, hdr);
-      TPX_LAUNCHED(c);
-      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortT0, hdr);
-      TPX_LAUNCHED(c);
+      if ((rc = window_sort<20, kSortT0, 512>(c, r, S, hdr))) return rc;  // D = 1024
     } else if (attempt == 1) {
-      r.sort_T = kSortTm;
-      const uint32_t sort_tiles = n_tiles_of(n, kSortTm);
-      k_window_sort<20, kSortTm><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
-                                                                                            c->height, S, hdr);
-      TPX_LAUNCHED(c);
-      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortTm, hdr);
-      TPX_LAUNCHED(c);
+      if ((rc = window_sort<20, kSortTm, 512>(c, r, S, hdr))) return rc;  // D = 2560
     } else if (attempt == 2) {
-      r.sort_T = kSortT1;
-      const uint32_t sort_tiles = n_tiles_of(n, kSortT1);
-      k_window_sort<20, kSortT1><<<sort_tiles, kWSortThreads, window_sort_smem<20>(), r.s>>>(hits, n, c->width,
-                                                                                            c->height, S, hdr);
-      TPX_LAUNCHED(c);
-      k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, n, kSortT1, hdr);
-      TPX_LAUNCHED(c);
+      if ((rc = window_sort<20, kSortT1, 512>(c, r, S, hdr))) return rc;  // D = 3072
     } else {
       if ((rc = sort_global(c, r))) return rc;
     }

@@ -13,6 +13,7 @@ import paper_2412_11809_b200 as tpx
 import tpxgen
 
 SIZES = {"tiny": None, "lowflux": None, "mixed": None, "heavyion": None, "timepix4": 250_000_000}
+MODE = os.environ.get("TPX_TILE_MODE", "auto")  # force a tile configuration (A/B)
 presets = sys.argv[1:] or list(SIZES)
 for preset in presets:
     p = tpxgen.PRESETS[preset]
@@ -22,6 +23,7 @@ for preset in presets:
     d = torch.from_numpy(h.view(np.uint8)).cuda()
     del h
     c = tpx.Clusterer(p["dt_max"], W, H)
+    c.set_tile_mode(MODE)
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
     feats = torch.empty((n, 64), dtype=torch.uint8, device="cuda")
     for _ in range(3):
@@ -43,7 +45,7 @@ for preset in presets:
                       "ms_per_run": round(ms, 3), "Mhit_s": round(n / ms / 1e3, 1),
                       "stage_ms": {kk: round(v, 3) for kk, v in st["stage_ms"].items()},
                       "tile_dense": st["tile_dense"], "sort_path": st["sort_path"],
-                      "open_hits_frac": round(st["open_hits"] / n, 4)}), flush=True)
+                      "open_hits_frac": round(st["open_hits"] / n, 4), "tile_mode": MODE}), flush=True)
     c.close()
     del d, labels, feats
     torch.cuda.empty_cache()

@@ -18,7 +18,7 @@ out = {}
 for r in rows[2:]:
     d = dict(zip(h, r))
     name = d["Kernel Name"]
-    stage = "tile_cc" if ("k_tile_cell" in name or "k_tile_cc" in name) else "sort" if "k_window_sort" in name else None
+    stage = "tile_cc" if ("k_tile_csr" in name or "k_tile_cell" in name or "k_tile_cc" in name) else "sort" if "k_window_sort" in name else None
     if not stage or stage in out:
         continue
     out[stage] = int(float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"]))
