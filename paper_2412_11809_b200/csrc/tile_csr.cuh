@@ -88,7 +88,7 @@ struct csr_smem {
   static constexpr size_t acc_end = accG + kA * 4;
   static constexpr size_t region_a0 = acc_end > off_end ? acc_end : off_end;
   static constexpr size_t region_a = (region_a0 + 15) & ~(size_t)15;
-  static constexpr size_t ent = region_a;                              // uint2 [kBackCap + kM], cell order
+  static constexpr size_t ent = region_a;                              // uint2 [kBackCap + kM], cell order (root_of u16 [kM] after the search)
   static constexpr size_t rec = ent + (size_t)(kBackCap + kM) * 8;     // uint2 [kM] (toa - base, y<<16|x)
   static constexpr size_t par = rec + kM * 8;                          // u32 [kM]
   static constexpr size_t crank = par + kM * 4;                        // u16 [kT] stage rank by root
@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   uint2* ent = reinterpret_cast<uint2*>(sp(SL::ent));
   uint2* rec = reinterpret_cast<uint2*>(sp(SL::rec));
   uint32_t* par = reinterpret_cast<uint32_t*>(sp(SL::par));
+  uint16_t* root_of = reinterpret_cast<uint16_t*>(sp(SL::ent));  // after the search: root of each staged hit
   uint16_t* crank = reinterpret_cast<uint16_t*>(sp(SL::crank));
   uint16_t* aslot = reinterpret_cast<uint16_t*>(sp(SL::aslot));
   uint8_t* hflag = reinterpret_cast<uint8_t*>(sp(SL::hflag));
@@ -404,34 +405,25 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   __syncthreads();
   TPX_PHASE(4);
 
-  // ---- flatten; multi-hit marks; open marks; cross pairs (halo hits that
-  // joined a tile component).  Roots are found first (reads only), stored
-  // after a barrier: no thread writes a parent another thread's walk reads.
-  uint32_t root[C::kStage];
+  // ---- flatten (one read-only root walk per staged hit into root_of[],
+  // which reuses the entry array: par is not written, so no walk races a
+  // store); multi-hit marks; open marks; cross pairs (forward-halo hits rooted
+  // in a tile component)
 #pragma unroll
   for (int s = 0; s < C::kStage; ++s) {
     const uint32_t l = threadIdx.x + s * kTh;
     uint32_t c = 0;
+    bool joined = false;
     if (l < m) {
       uint32_t nx;
       c = par[l];
       while (c != (nx = par[c])) c = nx;
-    }
-    root[s] = c;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < C::kStage; ++s) {
-    const uint32_t l = threadIdx.x + s * kTh;
-    const uint32_t c = root[s];
-    bool joined = false;
-    if (l < m) {
-      par[l] = c;
+      root_of[l] = (uint16_t)c;
       if (l < nt) {
         if (c != l) multi[c] = 1;
         if (hflag[l] & 1u) copen[c] = 1;
       } else {
-        joined = c < nt;  // a forward-halo hit rooted in a tile component
+        joined = c < nt;
         if (joined) copen[c] = 1;
       }
     }
@@ -444,7 +436,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   TPX_PHASE(6);
 
   // ---- compaction: stage rank of every root, accumulator slot of every
-  // multi-hit root (blocked order so ranks follow local index order)
+  // multi-hit root (blocked order so ranks follow local index order: records
+  // of a tile stay in label order, which keeps k_emit's stores coalesced)
   {
     uint32_t packed[C::kItems];
     uint32_t my = 0;
@@ -452,7 +445,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     for (int q = 0; q < C::kItems; ++q) {
       const uint32_t j = threadIdx.x * C::kItems + q;
       uint32_t v = 0;
-      if (j < nt && par[j] == j) v = 1u | ((uint32_t)multi[j] << 16);
+      if (j < nt && root_of[j] == j) v = 1u | ((uint32_t)multi[j] << 16);
       packed[q] = v;
       my += v;
     }
@@ -493,7 +486,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   for (int q = 0; q < C::kItems; ++q) {
     const uint32_t j = threadIdx.x + q * kTh;
     const bool valid = j < nt;
-    const uint32_t r = valid ? par[j] : 0xffffffffu;
+    const uint32_t r = valid ? (uint32_t)root_of[j] : 0xffffffffu;
     const uint32_t slot = valid ? aslot[r] : 0xffffu;
     const bool own = valid && tidx[q] < a.n_owned;
     const uint32_t prev = __shfl_up_sync(kFull, r, 1);
@@ -508,23 +501,22 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     const unsigned ownm = __ballot_sync(kFull, own) & run;
     const uint32_t len = e - s + 1;
     const uint32_t maxlen = __reduce_max_sync(kFull, slot != 0xffffu ? len : 1u);
-    uint32_t x = 0, y = 0, tot = 0, midx = valid ? tidx[q] : 0xffffffffu;
-    uint64_t stx = 0, sty = 0;
+    // 32-bit run sums (a run has <= 32 hits; x, y < 1024, ToT < 2^16): x + y
+    // packed as x | y << 16 (sum of x < 2^15), ToT*x and ToT*y < 2^31
+    uint32_t pxy = 0, tot = 0, stx = 0, sty = 0, midx = valid ? tidx[q] : 0xffffffffu;
     if (own) {
       const uint32_t xy = rec[j].y;
-      x = xy & 0xffffu;
-      y = xy >> 16;
+      pxy = xy;
       tot = (ttot2[q / 2] >> (16 * (q & 1))) & 0xffffu;
-      stx = (uint64_t)tot * x;
-      sty = (uint64_t)tot * y;
+      stx = tot * (xy & 0xffffu);
+      sty = tot * (xy >> 16);
     }
     for (uint32_t d = 1; d < maxlen; d <<= 1) {
-      const uint32_t x2 = __shfl_up_sync(kFull, x, d), y2 = __shfl_up_sync(kFull, y, d);
-      const uint32_t t2 = __shfl_up_sync(kFull, tot, d), m2 = __shfl_up_sync(kFull, midx, d);
-      const uint64_t sx2 = __shfl_up_sync(kFull, stx, d), sy2 = __shfl_up_sync(kFull, sty, d);
+      const uint32_t p2 = __shfl_up_sync(kFull, pxy, d), t2 = __shfl_up_sync(kFull, tot, d);
+      const uint32_t m2 = __shfl_up_sync(kFull, midx, d);
+      const uint32_t sx2 = __shfl_up_sync(kFull, stx, d), sy2 = __shfl_up_sync(kFull, sty, d);
       if (lane >= s + d) {
-        x += x2;
-        y += y2;
+        pxy += p2;
         tot += t2;
         midx = min(midx, m2);
         stx += sx2;
@@ -537,8 +529,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
       if (cnt) {
         atomicAdd(accN + slot, cnt);
         atomicAdd(accT + slot, tot);
-        atomicAdd(accX + slot, x);
-        atomicAdd(accY + slot, y);
+        atomicAdd(accX + slot, pxy & 0xffffu);
+        atomicAdd(accY + slot, pxy >> 16);
         add_u64_pair(accTX + slot, accTX + slot + C::kMulti, stx);
         add_u64_pair(accTY + slot, accTY + slot + C::kMulti, sty);
       }
@@ -560,7 +552,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     uint32_t r = 0, label = 0;
     bool is_root = false, open = false;
     if (v) {
-      r = par[j];
+      r = root_of[j];
       is_root = r == j;
       open = copen[r] != 0;
       const uint32_t sl = aslot[r];
