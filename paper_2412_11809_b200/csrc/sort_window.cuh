@@ -163,14 +163,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort(hit_src hits, uin
       __syncwarp();
     }
     __syncthreads();
-    // offsets in (digit, warp) order: thread d < kWRadix owns digit d
+    // offsets in (digit, warp) order, every thread busy: thread t owns digit
+    // t / kSplit and the kWarps / kSplit warps (t % kSplit)-th slice of it
     {
+      constexpr int kSplit = NT / kWRadix;
+      constexpr int kPer = kWarps / kSplit;
+      static_assert(kSplit * kWRadix == NT && kPer * kSplit == kWarps, "offset scan layout");
+      const uint32_t dd = threadIdx.x / kSplit, w0 = (threadIdx.x % kSplit) * kPer;
       uint32_t tot = 0;
-      if (threadIdx.x < kWRadix) {
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) tot += cnt[w * kWRadix + threadIdx.x];
-      }
-      uint32_t x = tot;  // inclusive scan of digit totals over threads 0..kWRadix-1
+#pragma unroll 4
+      for (int w = 0; w < kPer; ++w) tot += cnt[(w0 + w) * kWRadix + dd];
+      uint32_t x = tot;  // inclusive scan over threads (= (digit, slice) order)
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(kFull, x, o);
@@ -178,15 +181,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort(hit_src hits, uin
       }
       if (lane == 31) dsum[warp] = x;
       __syncthreads();
-      if (threadIdx.x < kWRadix) {
-        uint32_t basev = x - tot;
-        for (unsigned w2 = 0; w2 < warp; ++w2) basev += dsum[w2];
+      if (warp == 0) {
+        uint32_t v = lane < (unsigned)kWarps ? dsum[lane] : 0u;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-          const uint32_t c = cnt[w * kWRadix + threadIdx.x];
-          cnt[w * kWRadix + threadIdx.x] = basev;
-          basev += c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, v, o);
+          if (lane >= (unsigned)o) v += y;
         }
+        if (lane < (unsigned)kWarps) dsum[lane] = v;
+      }
+      __syncthreads();
+      uint32_t basev = x - tot + (warp ? dsum[warp - 1] : 0u);
+#pragma unroll 4
+      for (int w = 0; w < kPer; ++w) {
+        const uint32_t c = cnt[(w0 + w) * kWRadix + dd];
+        cnt[(w0 + w) * kWRadix + dd] = basev;
+        basev += c;
       }
     }
     __syncthreads();
