@@ -252,10 +252,11 @@ int tpx_cluster_set_profiling(tpx_cluster* ctx, int enable);
  * a window-density probe on the sorted stream choose; TPX_TILE_SPARSE (2048-hit
  * tiles, counting-sorted 2x2-pixel cell index with backward hooking for
  * sensors up to 1024 x 1024, else the linked-list cell index) /
- * TPX_TILE_DENSE (pixel hash, large halo) force one; TPX_TILE_COLUMN forces
- * the earlier column-bucket sparse kernel and TPX_TILE_CELL the linked-list
- * cell kernel (both kept for comparison).  Results are identical; only speed
- * differs -- the parity tests cover every mode.  Errors: INVALID_ARG. */
+ * TPX_TILE_DENSE (pixel hash, large halo) force one; TPX_TILE_CELL forces the
+ * linked-list cell kernel (kept for comparison and wide sensors).
+ * TPX_TILE_COLUMN (round 1's column-bucket kernel) is no longer available:
+ * INVALID_ARG.  Results are identical; only speed differs -- the parity
+ * tests cover every mode.  Errors: INVALID_ARG. */
 enum { TPX_TILE_AUTO = 0, TPX_TILE_SPARSE = 1, TPX_TILE_DENSE = 2, TPX_TILE_COLUMN = 3, TPX_TILE_CELL = 4 };
 int tpx_cluster_set_tile_mode(tpx_cluster* ctx, int mode);
 

@@ -70,7 +70,7 @@ _centroids = _proto("tpx_cluster_centroids", _int, _vp, _u64, _vp, _vp)
 _last_stats = _proto("tpx_cluster_last_stats", _int, _vp, ctypes.POINTER(RunStats))
 _set_profiling = _proto("tpx_cluster_set_profiling", _int, _vp, _int)
 _set_tile_mode = _proto("tpx_cluster_set_tile_mode", _int, _vp, _int)
-TILE_MODES = {"auto": 0, "sparse": 1, "dense": 2, "column": 3, "cell": 4}
+TILE_MODES = {"auto": 0, "sparse": 1, "dense": 2, "cell": 4}
 _stage_name = _proto("tpx_cluster_stage_name", ctypes.c_char_p, _int)
 _run_partial = _proto("tpx_cluster_run_partial", _int, _vp, _vp, _u64, _u64, _vp, _vp, _u64, ctypes.POINTER(_u64),
                       _vp, ctypes.c_size_t, _vp)
@@ -199,7 +199,8 @@ class Clusterer:
         _check(_set_profiling(self._h, int(on)), "tpx_cluster_set_profiling")
 
     def set_tile_mode(self, mode: str = "auto"):
-        """'auto' (density probe), 'sparse' or 'dense' tile configuration."""
+        """'auto' (density probe), 'sparse' (k_tile_csr), 'dense' (k_tile_cc) or
+        'cell' (k_tile_cell) tile configuration."""
         _check(_set_tile_mode(self._h, TILE_MODES[mode]), "tpx_cluster_set_tile_mode")
 
     def stats(self) -> dict:

@@ -173,8 +173,11 @@ __global__ void __launch_bounds__(kListThreads) k_open_labels(const srec* __rest
 
 // Window-density probe on the sorted stream: for 128 evenly spaced hits, the
 // number of later hits within dt_max (binary search).  The host uses it to
-// pick the tile configuration (tile_cc.cuh: tile_sparse / tile_dense).
+// pick the tile configuration (sparse tile_csr.cuh / dense tile_cc.cuh).
 constexpr int kProbeSamples = 128;
+// a sampled window longer than this counts as dense (the sparse kernels stage
+// 512 forward-halo hits; > 10 % of the samples above it selects k_tile_cc<dense>)
+constexpr uint32_t kDenseWindow = 640;
 __global__ void k_density_probe(const srec* __restrict__ S, uint64_t n, uint64_t dt, uint32_t* __restrict__ out) {
   const uint32_t k = threadIdx.x;
   if (k >= kProbeSamples) return;

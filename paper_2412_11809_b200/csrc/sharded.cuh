@@ -444,7 +444,7 @@ int tpx_cluster_run_sharded(tpx_cluster* c, tpx_comm* comm, const tpx_hit* local
       ((uintptr_t)labels_out & 3))
     return TPX_ERR_INVALID_ARG;
   if (c->variant != TPX_VARIANT_LOCAL) return TPX_ERR_UNSUPPORTED;
-  if (c->width > (uint32_t)kBuckets || (uint64_t)c->width * c->height + c->width > kMaxTilePixels)
+  if (c->width > (uint32_t)kMaxTileWidth || (uint64_t)c->width * c->height + c->width > kMaxTilePixels)
     return TPX_ERR_UNSUPPORTED;  // the global pipeline has no sharded emission
   if (n_local + kHaloCap >= 0xffffffffull) return TPX_ERR_TOO_MANY_HITS;
   const shard_layout SL = make_shard_layout(n_local, G);

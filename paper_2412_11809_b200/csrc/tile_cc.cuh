@@ -1,29 +1,36 @@
 // tile_cc.cuh -- A3 + A4 + A5 + A7 for one tile of the ToA-sorted stream,
 // entirely in shared memory (the B200 counterpart of the paper's Step 4 chunk
-// clustering, and Step 5 border stitching, l.173).
+// clustering, and Step 5 border stitching, l.173): the
+// dense-stream (heavy-ion) configuration, chosen by the window-density probe,
+// plus the helpers every tile kernel shares (tile_args, label stores, record
+// writes, block scan, shared-memory union-find).
 //
 // CTA k owns sorted positions [kT, kT+T).  It stages its tile plus the hits
 // within dt_max after it (forward halo) and before it (back halo):
-//   1. column index: the tile + forward-halo hits are bucketed by pixel
-//      column (counting sort, then ranked by time inside each bucket), so a
-//      hit's spatial neighbours live in 3 short, time-ordered buckets (the
-//      role the paper's 256x256 "last hit per pixel" matrix plays, l.171);
-//   2. window search: for every tile hit i and each neighbouring column
-//      bucket, the later hits j with toa_j - toa_i <= dt are tested for
-//      Chebyshev distance <= 1 (one packed subtraction, adjacent()); edges
-//      are buffered, then united in a shared-memory union-find (atomicCAS,
-//      larger root under smaller => root = earliest hit: the paper's
-//      time-invariant, l.219-221);
-//   3. every tile hit within dt of the previous tile looks back into the back
-//      halo; an edge there (or a back halo cut by its capacity) makes its
-//      component "open"; so does a forward window that leaves the staged halo
-//      (those hits are finished in global memory, finalize.cuh);
+//   1. pixel hash: every staged hit is pushed onto the list of its pixel in an
+//      open-addressing table (slot word = pixel << 14 | list head) -- a
+//      compact, per-CTA stand-in for the paper's 256x256 "last hit per pixel"
+//      matrix (l.171); back-halo hits join the lists with local indices
+//      m + k, so a tile hit learns from its own 9 lookups whether an earlier
+//      tile reaches it;
+//   2. search: for each of its 9 neighbouring pixels a tile hit takes only
+//      the FIRST later hit on that pixel within dt (later hits there reach it
+//      through their own same-pixel edge: the last-hit-per-pixel rule read
+//      forwards); edges are buffered, then united in a shared-memory
+//      union-find (atomicCAS, larger root under smaller => root = earliest
+//      hit: the paper's time-invariant, l.219-221);
+//   3. an edge into the back halo (or a back halo cut by its capacity) makes
+//      a component "open"; so does a forward window that leaves the staged
+//      halo (those hits are finished in global memory, finalize.cuh);
 //   4. forward-halo hits that joined a tile component become cross pairs for
 //      the global merge and make that component open;
 //   5. closed components are final: label = smallest input index, features
-//      reduced (warp REDUX + shared-memory atomics), labels_out written, one
-//      64-byte record staged; open components stage a partial record that the
-//      global pass merges.
+//      reduced over a member array grouped by component (one thread per small
+//      component, one warp per large one), labels_out written, one 64-byte
+//      record staged; open components stage a partial record that the global
+//      pass merges.
+// (Round 1's sparse column-bucket configuration of this kernel was removed in
+// round 2: the sparse path is tile_csr.cuh.)
 #pragma once
 #include <type_traits>
 
@@ -43,8 +50,7 @@ constexpr uint32_t kHeadMask = (1u << kHeadBits) - 1;
 constexpr uint32_t kPixEmpty = 0xffffffffu >> kHeadBits;  // empty hash slot key (pixel ids must be < 2^18 - 1)
 constexpr uint32_t kMaxTilePixels = kPixEmpty - 1;  // sensors with more pixels take the global path
 constexpr uint16_t kNil = 0xffffu;             // end of a pixel list
-constexpr int kBuckets = 1024;                 // sparse: one bucket per pixel column (wider sensors: global path)
-constexpr int kBucketCap = 512;                // sparse: longer buckets take the global path
+constexpr int kMaxTileWidth = 1024;            // sensors wider than this take the global pipeline
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr uint32_t kEdgeBuf = 8;               // buffered edges per thread and chunk
 
@@ -70,7 +76,6 @@ struct tile_cfg {
   static_assert(kFwdMax + 256 <= (1 << kHeadBits), "list heads: tile + halos fit kHeadBits");
   static_assert(kSlots >= 2 * kFwdMax, "hash load");
 };
-using tile_sparse = tile_cfg<1024, 256, 1024, 4, false>;
 using tile_dense = tile_cfg<4096, 1024, 4096, 1, true>;
 
 // Where the final label of a hit goes (sharded runs, sharded.cuh): labels of
@@ -228,42 +233,6 @@ __device__ __forceinline__ void set_label_bit(uint32_t* bitmap, uint32_t label) 
   atomicOr(bitmap + (label >> 5), 1u << (label & 31));
 }
 
-// Shared-memory carve-up of the column-bucket index (sparse configuration),
-// bytes.  Region A holds the column index during the clustering phase and the staged hits + member array + labels afterwards.
-template <class C>
-struct tile_smem_buckets {
-  static constexpr size_t kFwdMax = C::kFwdMax;
-  static constexpr size_t kTile = C::kTile;
-  static constexpr size_t kTileThreads = C::kThreads;
-  static constexpr size_t csort = 0;                                   // uint2 [kFwdMax] (toa - base, y<<16|x)
-  static constexpr size_t ckey = csort + (size_t)kFwdMax * 8;           // u32   [kFwdMax] y<<16 | local index
-  static constexpr size_t myrank = ckey + (size_t)kFwdMax * 4;          // u16   [kFwdMax]
-  static constexpr size_t region_a_index = myrank + (size_t)kFwdMax * 2;
-  static constexpr size_t region_a_reduce = (size_t)kTile * 24;
-  static constexpr size_t region_a = region_a_index > region_a_reduce ? region_a_index : region_a_reduce;
-  // reduction-phase aliases of region A
-  static constexpr size_t stile = 0;                                   // uint4 [kTile]
-  static constexpr size_t mem = stile + (size_t)kTile * 16;             // u16   [kTile]
-  static constexpr size_t big = mem + (size_t)kTile * 2;                // u16   [kTile]
-  static constexpr size_t mlabel = big + (size_t)kTile * 2;             // u32   [kTile]
-  static_assert(mlabel + (size_t)kTile * 4 <= region_a, "reduction arrays alias region A");
-  static constexpr size_t hb = region_a;                                // uint2 [kBackCap]
-  static constexpr size_t bs = hb + (size_t)kBackCap * 8;               // u32   [kBuckets + 4]
-  static constexpr size_t par = bs + ((size_t)kBuckets + 4) * 4;        // u32   [kFwdMax]
-  static constexpr size_t cltmp = par;                                  // u32   [kFwdMax] (alias, before par)
-  static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile/2] (u16 pairs)
-  static constexpr size_t crank = csize + (size_t)kTile * 2;            // u16   [kTile]
-  static constexpr size_t coff = crank + (size_t)kTile * 2;             // u16   [kTile]
-  static constexpr size_t eb = coff + (size_t)kTile * 2;                // u16   [kEdgeBuf * threads]
-  static constexpr size_t eb_bytes = (size_t)kEdgeBuf * kTileThreads * 2;
-  static constexpr size_t ccur = eb;                                    // u32   [kTile]   (alias)
-  static_assert((size_t)kTile * 4 <= eb_bytes, "cursor alias");
-  static_assert((size_t)kTileThreads * kEdgeBuf <= (size_t)kTile * 4, "edge owners alias crank + coff");
-  static constexpr size_t copen = eb + eb_bytes;                        // u8    [kTile]
-  static constexpr size_t hflag = copen + kTile;                        // u8    [kTile]
-  static constexpr size_t eslot = hflag + kTile;                       // u16   [kFwdMax] (dense staging)
-  static constexpr size_t total = eslot + (C::kRegStage ? 0 : (size_t)kFwdMax * 2);
-};
 // Shared-memory carve-up of the pixel-hash index (dense configuration), bytes.
 // Region A holds the hash index during the clustering phase and the staged hits + member array + labels afterwards.
 template <class C>
@@ -298,7 +267,7 @@ struct tile_smem_hash {
   static constexpr size_t total = hflag + kTile;
 };
 template <class C>
-using tile_smem_layout = typename std::conditional<C::kHash, tile_smem_hash<C>, tile_smem_buckets<C>>::type;
+using tile_smem_layout = tile_smem_hash<C>;
 template <class C>
 constexpr size_t tile_smem_bytes() {
   return tile_smem_layout<C>::total;
@@ -386,26 +355,15 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   extern __shared__ __align__(16) unsigned char sm[];
   // index arrays of the two configurations (only one set is used):
   // sparse -- column buckets ranked by (row, time); dense -- pixel hash
-  uint2* csort = nullptr;     // (toa - base, y<<16|x), bucket-sorted
-  uint32_t* ckey = nullptr;   // y << 16 | local index of csort entries
-  uint16_t* myrank = nullptr; // local index -> csort position
-  uint32_t* bs = nullptr;     // bucket counts, then bucket starts
-  uint32_t* cltmp = nullptr;  // unranked bucket entries (alias of par)
   uint32_t* tab = nullptr;    // pixel hash: pixel << 13 | list head, open addressing
   uint32_t* stoa = nullptr;   // toa - base by local index
   uint16_t* nxt = nullptr;    // next local index on the same pixel
   uint32_t* sxy = nullptr;    // y << 16 | x of tile hits
-  if constexpr (C::kHash) {
+  {
     tab = reinterpret_cast<uint32_t*>(sm + SL::tab);
     stoa = reinterpret_cast<uint32_t*>(sm + SL::stoa);
     nxt = reinterpret_cast<uint16_t*>(sm + SL::nxt);
     sxy = reinterpret_cast<uint32_t*>(sm + SL::sxy);
-  } else {
-    csort = reinterpret_cast<uint2*>(sm + SL::csort);
-    ckey = reinterpret_cast<uint32_t*>(sm + SL::ckey);
-    myrank = reinterpret_cast<uint16_t*>(sm + SL::myrank);
-    bs = reinterpret_cast<uint32_t*>(sm + SL::bs);
-    cltmp = reinterpret_cast<uint32_t*>(sm + SL::cltmp);
   }
   uint4* stile = reinterpret_cast<uint4*>(sm + SL::stile);      // tile hits (toa - base, xy, tot, idx)
   uint16_t* mem = reinterpret_cast<uint16_t*>(sm + SL::mem);    // member array grouped by component
@@ -422,7 +380,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   uint8_t* hflag = sm + SL::hflag;  // per tile hit: bit0 open mark, bit1 overflow
   __shared__ uint64_t s_meta[8];
   __shared__ uint32_t s_wsum[kTileThreads / 32];
-  __shared__ uint32_t s_chunk, s_bmax, s_nbig, s_bigq;
+  __shared__ uint32_t s_chunk, s_nbig, s_bigq;
 
   const uint64_t n = a.n, dt = a.dt;
   const srec* __restrict__ S = a.S;
@@ -446,7 +404,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       s_meta[3] = btrunc ? 1u : 0u;
       s_meta[5] = t0 ? srec_key_toa(S, t0 - 1) : 0;  // ToA of the previous tile's last hit
       s_chunk = 0;
-      s_bmax = 0;
       s_nbig = 0;
       s_bigq = 0;
     }
@@ -463,10 +420,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       s_meta[7] = ftrunc ? 2u : 0u;
     }
   }
-  if constexpr (C::kHash) {
+  {
     for (uint32_t b = threadIdx.x; b < (uint32_t)C::kSlots; b += kTileThreads) tab[b] = 0xffffffffu;
-  } else {
-    for (uint32_t b = threadIdx.x; b < kBuckets + 4; b += kTileThreads) bs[b] = 0;
   }
   for (uint32_t j = threadIdx.x; j < kTile; j += kTileThreads) {
     copen[j] = 0;
@@ -516,108 +471,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
     if (threadIdx.x == 0) a.comp_count[blockIdx.x] = nt;
   };
 
-  if constexpr (!C::kHash) {
-    // ---- stage: back halo, and tile + forward halo counted into column buckets
-    // (sparse config: the 8 staged words per thread stay in registers; dense
-    // config: slots go to shared memory and S is re-read from L2)
-    constexpr int kRegItems = C::kRegStage ? kStageItems : 1;
-    uint2 ev[kRegItems];
-    uint32_t eslot[kRegItems];
-    uint16_t* eslot_s = reinterpret_cast<uint16_t*>(sm + SL::eslot);
-    auto staged = [&](uint32_t l) {
-      const srec r = load_srec(S + t0 + l);
-      return make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-    };
-    if (!wide) {
-      for (uint32_t k = threadIdx.x; k < nb; k += kTileThreads) {
-        const srec r = load_srec(S + b0 + k);
-        hb[k] = make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
-      }
-      if constexpr (C::kRegStage) {
-  #pragma unroll
-        for (int q = 0; q < kStageItems; ++q) {
-          const uint32_t l = threadIdx.x + q * kTileThreads;
-          if (l < m) {
-            ev[q] = staged(l);
-            eslot[q] = atomicAdd(bs + (ev[q].y & 0xffffu), 1u);
-          }
-        }
-      } else {
-        for (uint32_t l = threadIdx.x; l < m; l += kTileThreads)
-          eslot_s[l] = (uint16_t)atomicAdd(bs + (staged(l).y & 0xffffu), 1u);
-      }
-    }
-    __syncthreads();
-    // exclusive scan of the bucket counts (in place), longest bucket
-    if (!wide) {
-      constexpr int PT = kBuckets / kTileThreads;  // buckets per thread
-      uint32_t cnts[PT];
-      uint32_t s = 0, mx = 0;
-  #pragma unroll
-      for (int i = 0; i < PT; ++i) {
-        cnts[i] = bs[threadIdx.x * PT + i];
-        s += cnts[i];
-        mx = max(mx, cnts[i]);
-      }
-      mx = __reduce_max_sync(kFull, mx);
-      if (lane == 0) atomicMax(&s_bmax, mx);
-      uint32_t tot;
-      uint32_t ex = tile_block_scan<kTileThreads>(s, &tot, s_wsum);
-  #pragma unroll
-      for (int i = 0; i < PT; ++i) {
-        bs[threadIdx.x * PT + i] = ex;
-        ex += cnts[i];
-      }
-      if (threadIdx.x == 0) bs[kBuckets] = m;
-    }
-    __syncthreads();
-    TPX_PHASE(1);
-    if (s_bmax > (uint32_t)kBucketCap) wide = true;  // degenerate column: global path
-
-
-    if (wide) {
-      run_wide();
-      return;
-    }
-    // ---- unordered scatter into column buckets, then rank inside each bucket
-    // by (row, time): key = y << 16 | local index (local index order = ToA order)
-    auto rank_in_bucket = [&](uint32_t l, uint2 e) {
-      const uint32_t b = e.y & 0xffffu;
-      const uint32_t key = (e.y & 0xffff0000u) | l;
-      const uint32_t s0 = bs[b], s1 = bs[b + 1];
-      uint32_t r = 0;
-      for (uint32_t p = s0; p < s1; ++p) r += cltmp[p] < key;
-      const uint32_t fin = s0 + r;
-      csort[fin] = e;
-      ckey[fin] = key;
-      myrank[l] = (uint16_t)fin;
-    };
-    if constexpr (C::kRegStage) {
-  #pragma unroll
-      for (int q = 0; q < kStageItems; ++q) {
-        const uint32_t l = threadIdx.x + q * kTileThreads;
-        if (l < m) cltmp[bs[ev[q].y & 0xffffu] + eslot[q]] = (ev[q].y & 0xffff0000u) | l;
-      }
-      __syncthreads();
-  #pragma unroll
-      for (int q = 0; q < kStageItems; ++q) {
-        const uint32_t l = threadIdx.x + q * kTileThreads;
-        if (l < m) rank_in_bucket(l, ev[q]);
-      }
-    } else {
-      for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
-        const uint2 e = staged(l);
-        cltmp[bs[e.y & 0xffffu] + eslot_s[l]] = (e.y & 0xffff0000u) | l;
-      }
-      __syncthreads();
-      for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) rank_in_bucket(l, staged(l));
-    }
-    __syncthreads();
-    for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) par[l] = l;  // par aliases cltmp
-    __syncthreads();
-
-  }
-  if constexpr (C::kHash) {
+  {}
+  {
     // ---- stage: back halo; tile + forward halo into a pixel hash index.  Each
     // occupied pixel owns one open-addressing slot (pixel << 13 | head) and a
     // list of its local indices threaded through nxt[] -- a compact, per-CTA
@@ -728,7 +583,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         else s_unite(par, j, lj);
       };
       bool back_near = false;
-      if constexpr (C::kHash) {
+      {
         xy = sxy[j];
         tj = stoa[j];
         const uint32_t x = xy & 0xffffu, y = xy >> 16;
@@ -754,49 +609,13 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
             if (best != 0xffffu && stoa[best] - tj <= dt32) edge(best);
           }
         }
-      } else {
-        const uint2 h = csort[myrank[j]];
-        xy = h.y;
-        tj = h.x;
-        const uint32_t x = h.y & 0xffffu, y = h.y >> 16;
-        const uint32_t xlo = x ? x - 1 : 0, xhi = x < wmax ? x + 1 : x;
-        const uint32_t ylo = y ? y - 1 : 0, yhi = y + 1;
-        const uint32_t k0 = (ylo << 16) | j;  // first key of interest: row ylo, index > j
-        for (uint32_t b = xlo; b <= xhi; ++b) {
-          uint32_t lo = bs[b], hi = bs[b + 1];
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (ckey[mid] <= k0) lo = mid + 1; else hi = mid;
-          }
-          uint32_t taken = 0xffffffffu;  // row whose first later hit was already taken
-          for (uint32_t p = lo; p < bs[b + 1]; ++p) {
-            const uint32_t k = ckey[p];
-            const uint32_t row = k >> 16;
-            if (row > yhi) break;
-            if (row == taken || (k & 0xffffu) <= j) continue;
-            taken = row;
-            if (csort[p].x - h.x <= dt32) edge(k & 0xffffu);
-          }
-        }
       }
       uint8_t fl = 0;
       if (ftrunc && first_unstaged <= base + tj + dt) fl = 3;  // window continues past the halo
-      if constexpr (C::kHash) {
+      {
         // adjacent back-halo hit within dt, or a truncated back halo whose
         // earliest staged hit (relative ToA 0) is still within dt
         if (back_near || (t0 > 0 && btrunc && tj <= dt32)) fl |= 1;
-      } else if (t0 > 0 && base + tj <= prev_last + dt) {  // could an earlier tile reach it?
-        bool found = false;
-        int lb = (int)nb - 1;
-        for (; lb >= 0; --lb) {
-          const uint2 g = hb[lb];
-          if (tj - g.x > dt32) break;
-          if (adjacent(xy, g.y)) {
-            found = true;
-            break;
-          }
-        }
-        if (found || (lb < 0 && btrunc)) fl |= 1;
       }
       hflag[j] = fl;
     }

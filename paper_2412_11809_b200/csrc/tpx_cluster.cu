@@ -158,8 +158,6 @@ static int ensure_cuda(tpx_cluster* c) {
                            (int)window_sort_kv_smem<12>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_csr<csr_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)csr_smem_bytes<csr_sparse>()) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tile_cc<tile_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tile_smem_bytes<tile_sparse>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cc<tile_dense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes<tile_dense>()) != cudaSuccess ||
       cudaFuncSetAttribute(k_tile_cell<cell_sparse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -287,7 +285,6 @@ struct run_ptrs {
   cudaStream_t s;
   bool dense;   // tile configuration chosen by the density probe
   uint32_t sort_T = kWSortTile;  // output tile of the sort that produced S (its borders are verified)
-  bool column;  // legacy column-bucket sparse kernel (TPX_TILE_COLUMN, comparison only)
   bool csr = false;  // counting-sorted cell index + backward hooking (tile_csr.cuh)
   // sharded runs (sharded.cuh): labels written as global indices into two
   // arrays, emission deferred until the boundary clusters are merged
@@ -425,9 +422,6 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   if (r.dense)
     k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
                             r.s>>>(a);
-  else if (r.column)
-    k_tile_cc<tile_sparse><<<n_tiles_of(r.n, tile_sparse::kTile), tile_sparse::kThreads,
-                             tile_smem_bytes<tile_sparse>(), r.s>>>(a);
   else if (r.csr) {
     static_assert(csr_sparse::kTile == cell_sparse::kTile && csr_sparse::kHalo == cell_sparse::kHalo, "shared bounds");
     const uint32_t nt = n_tiles_of(r.n, csr_sparse::kTile);
@@ -483,7 +477,7 @@ static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* 
   int rc = exclusive_scan(c, wcnt, L.nwords, wcnt, partials, (uint32_t*)&hdr->n_clusters, r.s);
   if (rc) return rc;
   if (r.capacity || removed_out) {
-    const uint32_t tile = r.dense ? tile_dense::kTile : r.column ? tile_sparse::kTile : cell_sparse::kTile;
+    const uint32_t tile = r.dense ? tile_dense::kTile : cell_sparse::kTile;
     k_emit<<<kListGrid, kEmitThreads, 0, r.s>>>(stage, comp_count, n_tiles_of(r.n, tile), tile, bitmap, wcnt, r.feats,
                                                 r.capacity, r.lm.own_off, removed_out, n_removed);
     TPX_LAUNCHED(c);
@@ -744,7 +738,8 @@ int tpx_cluster_set_profiling(tpx_cluster* c, int enable) {
 }
 
 int tpx_cluster_set_tile_mode(tpx_cluster* c, int mode) {
-  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_CELL) return TPX_ERR_INVALID_ARG;
+  // TPX_TILE_COLUMN (round 1's column-bucket kernel) was removed in round 2
+  if (!c || mode < TPX_TILE_AUTO || mode > TPX_TILE_CELL || mode == TPX_TILE_COLUMN) return TPX_ERR_INVALID_ARG;
   c->tile_mode = mode;
   return TPX_OK;
 }
@@ -871,13 +866,12 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
       }
       if (probe_on) {
         int big = 0;
-        for (int i = 0; i < kProbeSamples; ++i) big += hprobe[i] > (uint32_t)(tile_sparse::kHalo * 5 / 8);
+        for (int i = 0; i < kProbeSamples; ++i) big += hprobe[i] > kDenseWindow;
         r.dense = big * 10 > kProbeSamples;  // > 10 % of the samples have windows near the sparse halo
       } else {
         r.dense = c->tile_mode == TPX_TILE_DENSE;
       }
-      r.column = c->tile_mode == TPX_TILE_COLUMN;
-      r.csr = !r.dense && !r.column && c->tile_mode != TPX_TILE_CELL && c->width <= kCsrMaxCoord + 1 &&
+      r.csr = !r.dense && c->tile_mode != TPX_TILE_CELL && c->width <= kCsrMaxCoord + 1 &&
               c->height <= kCsrMaxCoord + 1;
       c->stats.tile_dense = r.dense ? 1 : 0;
     }
@@ -886,7 +880,7 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
     // the tile kernel indexes one bucket per pixel column (sparse) or packs
     // pixel ids in 20 bits (dense): larger sensors take the global pipeline
     const bool big_sensor =
-        c->width > (uint32_t)kBuckets || (uint64_t)c->width * c->height + c->width > kMaxTilePixels;
+        c->width > (uint32_t)kMaxTileWidth || (uint64_t)c->width * c->height + c->width > kMaxTilePixels;
     c->bitmap_valid = !(attempt == kRadixAttempt + 1 || big_sensor);
     if (r.defer_emit && !c->bitmap_valid) return TPX_ERR_UNSUPPORTED;  // sharded: tile path only
     rc = c->bitmap_valid ? cluster_sorted(c, r) : cluster_global(c, r);

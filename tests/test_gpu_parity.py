@@ -108,7 +108,7 @@ def test_presets(tpx, preset, n):
     _assert_parity(tpx, h, p["dt_max"], W, H, ctx=preset)
 
 
-@pytest.mark.parametrize("mode", ["sparse", "dense", "column", "cell"])
+@pytest.mark.parametrize("mode", ["sparse", "dense", "cell"])
 @pytest.mark.parametrize("preset,n", [("mixed", 1_000_000), ("heavyion", 1_000_000), ("lowflux", 500_000),
                                       ("timepix4", 1_000_000)])
 def test_forced_tile_modes(tpx, mode, preset, n):
@@ -120,7 +120,7 @@ def test_forced_tile_modes(tpx, mode, preset, n):
     assert st["tile_dense"] == (mode == "dense")
 
 
-@pytest.mark.parametrize("mode", ["sparse", "column", "cell"])
+@pytest.mark.parametrize("mode", ["sparse", "cell"])
 def test_forced_sparse_small_and_fuzz(tpx, mode):
     """Sparse kernels on small and odd sensors (cell aliasing: widths/heights
     above 256 share cell slots modulo 256 pixels), tiny dt and ragged sizes."""
