@@ -46,7 +46,8 @@
 
 namespace tpx {
 
-template <int kTileHits, int kThreadsPerCta, int kHaloHits, int kMinBlocks>
+template <int kTileHits, int kThreadsPerCta, int kHaloHits, int kMinBlocks, int kCellW = 1, int kCellH = 1,
+          int kCellBx = 7, int kCellBy = 7>
 struct csr_cfg {
   static constexpr int kTile = kTileHits;
   static constexpr int kThreads = kThreadsPerCta;
@@ -55,8 +56,12 @@ struct csr_cfg {
   static constexpr int kFwdMax = kTile + kHaloHits;          // tile + forward halo (local index l)
   static constexpr int kStage = kFwdMax / kThreads;          // staged hits per thread
   static constexpr int kBlocks = kMinBlocks;
-  static constexpr int kCellBits = 7;                        // 2^7 x 2^7 cells of 2x2 pixels
-  static constexpr int kCells = 1 << (2 * kCellBits);
+  // cells of 2^kCellW x 2^kCellH pixels (both >= 2: a 3-pixel range spans at
+  // most two cells), 2^kCellBx x 2^kCellBy of them (coordinates alias modulo
+  // the grid; the packed compare checks true coordinates)
+  static constexpr int kCwShift = kCellW, kChShift = kCellH, kCbx = kCellBx, kCby = kCellBy;
+  static_assert(kCellW >= 1 && kCellH >= 1, "cells at least 2 pixels wide and high");
+  static constexpr int kCells = 1 << (kCellBx + kCellBy);
   static constexpr int kMulti = kTile / 2;                   // components with >= 2 tile hits
   static constexpr int kCntWords = kCells / 2;               // two 16-bit counters per word
   static constexpr int kCntPerThread = kCntWords / kThreads; // scan: words per thread
@@ -65,7 +70,7 @@ struct csr_cfg {
   static_assert(kCntWords % (4 * kThreads) == 0, "scan: uint4 words per thread");
   static_assert(kTile % ::tpx::kTile == 0 && kTile <= kMaxTile, "stage slots");
 };
-using csr_sparse = csr_cfg<2048, 512, TPX_CELL_HALO, 2>;
+using csr_sparse = csr_cfg<2048, 512, TPX_CELL_HALO, 2>;                 // 2x2-pixel cells, 128 x 128
 constexpr uint32_t kCsrMaxCoord = 1023;  // 10-bit coordinate fields in the entry word
 
 // Shared-memory carve-up, bytes.  Region A holds the cell counters / offsets
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   using SL = csr_smem<C>;
   constexpr int kT = C::kTile;
   constexpr int kTh = C::kThreads;
-  constexpr uint32_t kCellMask = (1u << C::kCellBits) - 1;
+  constexpr uint32_t kMaskX = (1u << C::kCbx) - 1, kMaskY = (1u << C::kCby) - 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(smem_raw));
   auto sp = [&](size_t off) { return __cvta_shared_to_generic(sbase + (uint32_t)off); };
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   const uint32_t dt32 = dt > 0xffffffffull ? 0xffffffffu : (uint32_t)dt;
   const uint32_t wmax = a.width - 1, hmax = a.height - 1;
   auto cell_of = [&](uint32_t xy) {
-    return ((((xy >> 16) >> 1) & kCellMask) << C::kCellBits) | (((xy & 0xffffu) >> 1) & kCellMask);
+    return ((((xy >> 16) >> C::kChShift) & kMaskY) << C::kCbx) | (((xy & 0xffffu) >> C::kCwShift) & kMaskX);
   };
 
   // ---- stage: rec[] in local-index order; count every staged hit into its
@@ -317,10 +322,10 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
       // unless the row's two cells alias across the 256-pixel wrap (sensors
       // wider than 256 only; handled below)
       const uint32_t x = xy & 0xffffu, y = xy >> 16;
-      const uint32_t cx0 = (x ? x - 1 : 0) >> 1, cx1 = min(x + 1, wmax) >> 1;
-      const uint32_t cy0 = (y ? y - 1 : 0) >> 1, cy1 = min(y + 1, hmax) >> 1;
-      const uint32_t r0 = (cy0 & kCellMask) << C::kCellBits, r1 = (cy1 & kCellMask) << C::kCellBits;
-      const uint32_t k0 = cx0 & kCellMask, k1 = cx1 & kCellMask;
+      const uint32_t cx0 = (x ? x - 1 : 0) >> C::kCwShift, cx1 = min(x + 1, wmax) >> C::kCwShift;
+      const uint32_t cy0 = (y ? y - 1 : 0) >> C::kChShift, cy1 = min(y + 1, hmax) >> C::kChShift;
+      const uint32_t r0 = (cy0 & kMaskY) << C::kCbx, r1 = (cy1 & kMaskY) << C::kCbx;
+      const uint32_t k0 = cx0 & kMaskX, k1 = cx1 & kMaskX;
       const bool two_y = act && cy1 != cy0;
       const bool wrap = act && cx1 != cx0 && k1 != k0 + 1;
       const uint32_t kend = k0 + ((cx1 != cx0 && !wrap) ? 2u : 1u);
