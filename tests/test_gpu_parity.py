@@ -214,6 +214,21 @@ def test_disorder_stress(tpx):
     assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
 
 
+@pytest.mark.parametrize("n,toa_max", [(12_289, 1 << 14), (40_961, (1 << 23) + 5), (100_003, (1 << 31) - 3),
+                                         ((1 << 20) + 7, 1 << 20), (300_001, (1 << 24) + 1)])
+def test_radix_fallback_edges(tpx, n, toa_max):
+    """The global radix sort (radix_onesweep.cuh): unordered input (the window
+    sort cannot hold its displacement bound, so the fallback runs), sizes that
+    leave a partial last 4096-key tile, and ToA ranges needing 2, 3 and 4
+    8-bit passes; 16x16 sensor so clusters are many and large."""
+    rng = np.random.default_rng(n)
+    h = tpxgen.random_small(rng, n, 16, 16, toa_max)
+    c, gl, gf, k = _fresh(tpx, h, 64, 16, 16)
+    assert c.stats()["sort_path"] == 1
+    rl, rf = oracle.cluster(h, 64, 16, 16)
+    assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
+
+
 def test_sort_attempt_memory(tpx):
     """A failed displacement bound is detected right after the sort (no
     clustering pass on a wrong order) and the context starts at the attempt
