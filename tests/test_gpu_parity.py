@@ -145,6 +145,18 @@ def test_forced_sparse_small_and_fuzz(tpx, mode):
         _assert_parity(tpx, h, dt, W, H, ctx=f"{mode} wide-sensor trial {trial}", tile_mode=mode)
     for n in (2047, 2048, 2049, 4097, 65537):
         _assert_parity(tpx, tpxgen.generate("mixed", n_hits=n), 320, ctx=f"{mode} n={n}", tile_mode=mode)
+    # widths / heights at the cell-grid wrap (256) and the CSR coordinate
+    # limit (1023; 1025 falls back to the linked-list cell kernel)
+    for W, H in ((257, 9), (511, 513), (512, 257), (1023, 1024), (1024, 1023), (1025, 31), (31, 1025)):
+        nh = 30_000
+        h = np.zeros(nh, dtype=tpxgen.HIT_DTYPE)
+        cx, cy = rng.integers(0, W, nh // 6), rng.integers(0, H, nh // 6)
+        k = rng.integers(0, nh // 6, nh)
+        h["x"] = np.clip(cx[k] + rng.integers(-1, 2, nh), 0, W - 1)
+        h["y"] = np.clip(cy[k] + rng.integers(-1, 2, nh), 0, H - 1)
+        h["toa"] = np.sort(rng.integers(0, 40 * nh, nh))
+        h["tot"] = rng.integers(1, 1024, nh)
+        _assert_parity(tpx, h, 320, W, H, ctx=f"{mode} edge sensor {W}x{H}", tile_mode=mode)
 
 
 def test_forced_dense_small_and_fuzz(tpx):
