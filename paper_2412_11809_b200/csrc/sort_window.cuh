@@ -238,6 +238,174 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort(hit_src hits, uin
   }
 }
 
+// Packed variant for windows whose key range fits 18 bits (every stream of
+// >= ~32 Mhit/s at 13312-hit windows): a key and its 14-bit window position
+// travel as one word (key << 14 | position), ranks as 16-bit halves, so the
+// register arrays shrink from 2 x IT to 1.5 x IT words -- a 26-key window
+// (W = 13312) fits 64 registers, which lowers the window redundancy (8192 +
+// 2 x 2560 = 13312 for the Timepix4-rate D = 2560 attempt instead of 5120 +
+// 2 x 2560 = 10240).  A window whose range is wider flags err bit 3 and the
+// run takes the unpacked kernel.
+constexpr int kPackPosBits = 14;
+constexpr int kPackKeyBits = 32 - kPackPosBits;
+
+template <int IT, int T, int NT = kWSortThreads>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hits, uint64_t n, uint32_t width,
+                                                                      uint32_t height, srec* __restrict__ out,
+                                                                      dev_hdr* hdr) {
+  using C = wsort_cfg<IT, T, NT>;
+  constexpr int kWarps = NT / 32;
+  static_assert(C::W <= (1 << kPackPosBits), "window positions fit the packed field");
+  static_assert(kWRadix <= NT && 2 * kWDigitBits >= kPackKeyBits, "two passes cover the packed key");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);  // [W] key << 14 | position
+  uint32_t* cnt = skey + C::W;                             // [kWRadix * warps]
+  __shared__ unsigned long long red[33];
+  __shared__ uint32_t dsum[NT / 32];
+
+  const uint64_t k0 = (uint64_t)blockIdx.x * T;
+  const uint64_t ws = k0 > (uint64_t)C::D ? k0 - C::D : 0;
+  const uint64_t we = min(n, k0 + T + C::D);
+  const uint32_t m = (uint32_t)(we - ws);
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+  const uint64_t org = (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(hits + ws)) - 0x80000000ull;
+  uint32_t pk[IT];
+  uint32_t mn = 0xffffffffu, mx = 0;
+  unsigned bad = 0, far = 0;
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+    pk[r] = 0;
+    if (p < m) {
+      hit4 h = load_hit(hits + (ws + p));
+      const uint64_t d = h.toa - org;
+      far |= (d >> 32) != 0;
+      pk[r] = (uint32_t)d;
+      mn = min(mn, pk[r]);
+      mx = max(mx, pk[r]);
+      bad |= (h.x >= width) | (h.y >= height) | (h.toa >> 48 != 0);
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->err, 1u);
+  const uint32_t kmin = (uint32_t)block_min_u64(mn, red);
+  const uint32_t kmax = (uint32_t)block_max_u64(mx, red);
+  if (__syncthreads_or(far)) {  // window wider than 2^31 ticks: leave it to the fallback
+    if (threadIdx.x == 0) {
+      atomicAdd(&hdr->sort_bad, 1u);
+      atomicOr(&hdr->err, 4u);
+    }
+    return;
+  }
+  const uint32_t range = kmax - kmin;
+  const int bits = range ? 32 - __clz(range) : 0;
+  if (bits > kPackKeyBits) {  // too wide for the packed word: the unpacked kernel takes this run
+    if (threadIdx.x == 0) {
+      atomicAdd(&hdr->sort_bad, 1u);
+      atomicOr(&hdr->err, 8u);
+    }
+    return;
+  }
+  const int passes = (bits + kWDigitBits - 1) / kWDigitBits;
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+    pk[r] = ((pk[r] - kmin) << kPackPosBits) | p;
+  }
+  uint32_t rk2[(IT + 1) / 2];  // rank within the warp's digit run, two 16-bit halves per word
+  for (int pass = 0; pass < passes || pass == 0; ++pass) {
+    const int shift = kPackPosBits + pass * kWDigitBits;
+    for (int i = threadIdx.x; i < kWRadix * kWarps; i += NT) cnt[i] = 0;
+    __syncthreads();
+    uint32_t* wc = cnt + warp * kWRadix;
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+      const bool valid = p < m;
+      const unsigned d = valid ? (pk[r] >> shift) & (kWRadix - 1) : (unsigned)kWRadix;
+      const unsigned peers = __match_any_sync(kFull, d);
+      uint32_t b = 0;
+      if (valid) b = wc[d];
+      const uint32_t rank = b + __popc(peers & lanemask_lt());
+      if (r & 1) rk2[r / 2] |= rank << 16;
+      else rk2[r / 2] = rank;
+      __syncwarp();
+      if (valid && (__ffs(peers) - 1) == (int)lane) wc[d] = b + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      constexpr int kSplit = NT / kWRadix;
+      constexpr int kPer = kWarps / kSplit;
+      const uint32_t dd = threadIdx.x / kSplit, w0 = (threadIdx.x % kSplit) * kPer;
+      uint32_t tot = 0;
+#pragma unroll 4
+      for (int w = 0; w < kPer; ++w) tot += cnt[(w0 + w) * kWRadix + dd];
+      uint32_t x = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= (unsigned)o) x += y;
+      }
+      if (lane == 31) dsum[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t v = lane < (unsigned)kWarps ? dsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, v, o);
+          if (lane >= (unsigned)o) v += y;
+        }
+        if (lane < (unsigned)kWarps) dsum[lane] = v;
+      }
+      __syncthreads();
+      uint32_t basev = x - tot + (warp ? dsum[warp - 1] : 0u);
+#pragma unroll 4
+      for (int w = 0; w < kPer; ++w) {
+        const uint32_t c = cnt[(w0 + w) * kWRadix + dd];
+        cnt[(w0 + w) * kWRadix + dd] = basev;
+        basev += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+      if (p < m) {
+        const unsigned d = (pk[r] >> shift) & (kWRadix - 1);
+        skey[wc[d] + ((rk2[r / 2] >> (16 * (r & 1))) & 0xffffu)] = pk[r];
+      }
+    }
+    __syncthreads();
+    if (pass + 1 < passes) {
+#pragma unroll
+      for (int r = 0; r < IT; ++r) {
+        const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
+        if (p < m) pk[r] = skey[p];
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- write the middle T records (window-local ranks [k0-ws, k0-ws+T))
+  const uint32_t ofs = (uint32_t)(k0 - ws);
+  const uint32_t cnt_out = (uint32_t)min((uint64_t)T, n - k0);
+  for (uint32_t j = threadIdx.x; j < cnt_out; j += NT) {
+    const uint64_t gi = ws + (skey[ofs + j] & ((1u << kPackPosBits) - 1));
+    hit4 h = load_hit(hits + gi);
+    srec r;
+    r.tt = (h.toa << 16) | h.tot;
+    r.xy = (h.y << 16) | h.x;
+    r.idx = (uint32_t)gi;
+    store_srec(out + k0 + j, r);
+  }
+}
+
+template <int IT, int NT = kWSortThreads>
+constexpr size_t window_sort_packed_smem() {
+  return (size_t)wsort_cfg<IT, kWSortTile, NT>::W * 4 + (size_t)kWRadix * (NT / 32) * 4;
+}
+
 template <int IT, int NT = kWSortThreads>
 constexpr size_t window_sort_smem() {
   return (size_t)wsort_cfg<IT, kWSortTile, NT>::W * 6 + (size_t)kWRadix * (NT / 32) * 4;

@@ -355,6 +355,28 @@ static int sort_global(tpx_cluster* c, const run_ptrs& r) {
 static int emit_sorted(tpx_cluster* c, const run_ptrs& r, tpx_cluster_features* removed_out,
                        unsigned long long* n_removed);
 
+// One packed windowed-sort attempt (sort_window.cuh k_window_sort_packed).
+template <int IT, int T>
+static int window_sort_packed(tpx_cluster* c, run_ptrs& r, srec* S, dev_hdr* hdr) {
+  constexpr int NT = kWSortThreads;
+  static_assert(window_sort_packed_smem<IT, NT>() <= 113 * 1024, "two CTAs per SM");
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_window_sort_packed<IT, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)window_sort_packed_smem<IT, NT>()) != cudaSuccess)
+      return TPX_ERR_CUDA;
+    attr = true;
+  }
+  r.sort_T = T;
+  const uint32_t sort_tiles = n_tiles_of(r.n, T);
+  k_window_sort_packed<IT, T, NT><<<sort_tiles, NT, window_sort_packed_smem<IT, NT>(), r.s>>>(
+      r.hits, r.n, c->width, c->height, S, hdr);
+  TPX_LAUNCHED(c);
+  k_sort_check<<<grid_for(sort_tiles, 256), 256, 0, r.s>>>(S, r.n, T, hdr);
+  TPX_LAUNCHED(c);
+  return TPX_OK;
+}
+
 // One windowed-sort attempt (sort_window.cuh): T outputs per CTA from a
 // window of IT * NT hits (D = (IT * NT - T) / 2), then the border check.
 template <int IT, int T, int NT>
@@ -810,10 +832,13 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
 
   int rc;
   const hit_src hits = r.hits;
-  // attempts 0 / 1 / 2: windowed sort with D = 1024 / 2560 / 3072;
-  // attempt 3: global radix sort; attempt 4: global union-find pipeline
-  // (internal fallback)
-  constexpr int kRadixAttempt = 3;
+  // windowed sorts: 0 D = 1024 (10240-hit window, 8192 outputs), 1 packed
+  // D = 2560 (13312 / 8192: high-rate streams, whose windows span < 2^18
+  // ticks), 2 D = 2560 (10240 / 5120: wider windows), 3 D = 3072 (10240 /
+  // 4096); 4 global radix sort; 5 global union-find pipeline (internal
+  // fallback).  (A packed D = 1024 attempt does not fit the 40 Mhit/s mixed
+  // stream: ~half of its 13312-hit windows span more than 2^18 ticks.)
+  constexpr int kRadixAttempt = 4;
   constexpr int kSortProbeRuns = 64;
   if (c->sort_start > 0 && ++c->runs_at_start > kSortProbeRuns) {
     c->sort_start = 0;
@@ -822,15 +847,19 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
   const int first_attempt = c->sort_start;
   nvtx_range nv_run("tpx:run");
   for (int attempt = first_attempt; attempt <= kRadixAttempt + 1; ++attempt) {
-    nvtx_range nv_sort(attempt == 0 ? "tpx:sort_window" : attempt == 1 ? "tpx:sort_window_d2560"
-                                                       : attempt == 2 ? "tpx:sort_window_d3072" : "tpx:sort_fallback");
+    nvtx_range nv_sort(attempt == 0   ? "tpx:sort_window"
+                       : attempt <= 2 ? "tpx:sort_window_d2560"
+                       : attempt == 3 ? "tpx:sort_window_d3072"
+                                      : "tpx:sort_fallback");
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {
       if ((rc = window_sort<20, kSortT0, 512>(c, r, S, hdr))) return rc;  // D = 1024
     } else if (attempt == 1) {
-      if ((rc = window_sort<20, kSortTm, 512>(c, r, S, hdr))) return rc;  // D = 2560
+      if ((rc = window_sort_packed<26, 8192>(c, r, S, hdr))) return rc;  // D = 2560
     } else if (attempt == 2) {
+      if ((rc = window_sort<20, kSortTm, 512>(c, r, S, hdr))) return rc;  // D = 2560
+    } else if (attempt == 3) {
       if ((rc = window_sort<20, kSortT1, 512>(c, r, S, hdr))) return rc;  // D = 3072
     } else {
       if ((rc = sort_global(c, r))) return rc;
@@ -858,6 +887,9 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
         continue;
       }
       if (attempt < kRadixAttempt && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
+        // a packed attempt that failed on displacement (not on its 18-bit key
+        // range) skips the unpacked attempt with the same bound
+        if (attempt == 1 && !(c->host_hdr->err & 8u)) ++attempt;
         if (attempt + 1 > c->sort_start) {
           c->sort_start = attempt + 1;
           c->runs_at_start = 0;
