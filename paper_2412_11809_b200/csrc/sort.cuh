@@ -13,7 +13,7 @@ struct dev_hdr {
   unsigned long long toa_max;
   unsigned int err;          // bit 0: coordinate / ToA range violation; bit 1: internal;
                              // bit 2: a sort window spans >= 2^32 ticks (windowed sort impossible)
-                             // bit 3: a packed sort window's ToA range exceeds 18 bits
+                             // bit 3: a packed sort window's ToA range exceeds 28 bits
   unsigned int sort_bad;     // windowed-sort verification failures
   unsigned long long n_clusters;
   unsigned long long n_pairs;       // cross-tile union pairs

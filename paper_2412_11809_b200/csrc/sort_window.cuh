@@ -238,16 +238,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort(hit_src hits, uin
   }
 }
 
-// Packed variant for windows whose key range fits 18 bits (every stream of
-// >= ~32 Mhit/s at 13312-hit windows): a key and its 14-bit window position
-// travel as one word (key << 14 | position), ranks as 16-bit halves, so the
-// register arrays shrink from 2 x IT to 1.5 x IT words -- a 26-key window
-// (W = 13312) fits 64 registers, which lowers the window redundancy (8192 +
-// 2 x 2560 = 13312 for the Timepix4-rate D = 2560 attempt instead of 5120 +
-// 2 x 2560 = 10240).  A window whose range is wider flags err bit 3 and the
-// run takes the unpacked kernel.
+// Packed variant: the registers hold one word per key instead of two.  Pass 0
+// ranks the plain keys (the payload, the window position, is implicit in the
+// (warp, round, lane) layout) and scatters (key >> 9) << 14 | position; later
+// passes take their digit from that word.  Ranks are 16-bit halves.  So the
+// register arrays are 1.5 x IT words, a 26-key window (W = 13312) fits 64
+// registers, and the window redundancy drops (D = 1024: 11264 outputs of
+// 13312 instead of 8192 of 10240; D = 2560: 8192 instead of 5120).  Key
+// ranges up to 10 + 18 = 28 bits (2.7e8 ticks, 0.42 s) fit; a wider window
+// flags err bit 3 and the run takes the unpacked kernel.  Digits are 10 bits
+// wide with 16-bit counters (ranks and offsets are < 2^16 in a 13312-hit
+// window), so a 20-bit window range -- the 40 Mhit/s mixed stream's 13312-hit
+// windows span up to ~3.2e5 ticks -- still sorts in two passes.
 constexpr int kPackPosBits = 14;
-constexpr int kPackKeyBits = 32 - kPackPosBits;
+constexpr int kPDigitBits = 10;
+constexpr int kPRadix = 1 << kPDigitBits;
+constexpr int kPackKeyBits = kPDigitBits + 32 - kPackPosBits;
 
 template <int IT, int T, int NT = kWSortThreads>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hits, uint64_t n, uint32_t width,
@@ -256,10 +262,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
   using C = wsort_cfg<IT, T, NT>;
   constexpr int kWarps = NT / 32;
   static_assert(C::W <= (1 << kPackPosBits), "window positions fit the packed field");
-  static_assert(kWRadix <= NT && 2 * kWDigitBits >= kPackKeyBits, "two passes cover the packed key");
+  static_assert(3 * kPDigitBits >= kPackKeyBits && C::W < 65536, "three passes; 16-bit counters");
+  static_assert(kPRadix % NT == 0, "whole digits per scan thread");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* skey = reinterpret_cast<uint32_t*>(smem_raw);  // [W] key << 14 | position
-  uint32_t* cnt = skey + C::W;                             // [kWRadix * warps]
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(skey + C::W);  // [kPRadix * warps], warp-major
   __shared__ unsigned long long red[33];
   __shared__ uint32_t dsum[NT / 32];
 
@@ -299,30 +306,31 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
   }
   const uint32_t range = kmax - kmin;
   const int bits = range ? 32 - __clz(range) : 0;
-  if (bits > kPackKeyBits) {  // too wide for the packed word: the unpacked kernel takes this run
+  if (bits > kPackKeyBits) {  // too wide for the packed words: the unpacked kernel takes this run
     if (threadIdx.x == 0) {
       atomicAdd(&hdr->sort_bad, 1u);
       atomicOr(&hdr->err, 8u);
     }
     return;
   }
-  const int passes = (bits + kWDigitBits - 1) / kWDigitBits;
+  const int passes = (bits + kPDigitBits - 1) / kPDigitBits;
 #pragma unroll
-  for (int r = 0; r < IT; ++r) {
-    const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
-    pk[r] = ((pk[r] - kmin) << kPackPosBits) | p;
-  }
+  for (int r = 0; r < IT; ++r) pk[r] -= kmin;  // pass 0: plain keys
   uint32_t rk2[(IT + 1) / 2];  // rank within the warp's digit run, two 16-bit halves per word
   for (int pass = 0; pass < passes || pass == 0; ++pass) {
-    const int shift = kPackPosBits + pass * kWDigitBits;
-    for (int i = threadIdx.x; i < kWRadix * kWarps; i += NT) cnt[i] = 0;
+    // digit position: plain key in pass 0, packed word (key >> 9) << 14 | pos after
+    const int shift = pass == 0 ? 0 : kPackPosBits + (pass - 1) * kPDigitBits;
+    {
+      uint4* c4 = reinterpret_cast<uint4*>(cnt);
+      for (int i = threadIdx.x; i < kPRadix * kWarps / 8; i += NT) c4[i] = make_uint4(0, 0, 0, 0);
+    }
     __syncthreads();
-    uint32_t* wc = cnt + warp * kWRadix;
+    uint16_t* wc = cnt + warp * kPRadix;
 #pragma unroll
     for (int r = 0; r < IT; ++r) {
       const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
       const bool valid = p < m;
-      const unsigned d = valid ? (pk[r] >> shift) & (kWRadix - 1) : (unsigned)kWRadix;
+      const unsigned d = valid ? (pk[r] >> shift) & (kPRadix - 1) : (unsigned)kPRadix;
       const unsigned peers = __match_any_sync(kFull, d);
       uint32_t b = 0;
       if (valid) b = wc[d];
@@ -330,17 +338,19 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
       if (r & 1) rk2[r / 2] |= rank << 16;
       else rk2[r / 2] = rank;
       __syncwarp();
-      if (valid && (__ffs(peers) - 1) == (int)lane) wc[d] = b + __popc(peers);
+      if (valid && (__ffs(peers) - 1) == (int)lane) wc[d] = (uint16_t)(b + __popc(peers));
       __syncwarp();
     }
     __syncthreads();
     {
-      constexpr int kSplit = NT / kWRadix;
-      constexpr int kPer = kWarps / kSplit;
-      const uint32_t dd = threadIdx.x / kSplit, w0 = (threadIdx.x % kSplit) * kPer;
+      // offsets in (digit, warp) order: thread t owns digits [t * kDpt, (t + 1) * kDpt)
+      constexpr int kDpt = kPRadix / NT;
+      const uint32_t d0 = threadIdx.x * kDpt;
       uint32_t tot = 0;
+#pragma unroll
+      for (int dd = 0; dd < kDpt; ++dd)
 #pragma unroll 4
-      for (int w = 0; w < kPer; ++w) tot += cnt[(w0 + w) * kWRadix + dd];
+        for (int w = 0; w < kWarps; ++w) tot += cnt[w * kPRadix + d0 + dd];
       uint32_t x = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -360,20 +370,23 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
       }
       __syncthreads();
       uint32_t basev = x - tot + (warp ? dsum[warp - 1] : 0u);
+#pragma unroll
+      for (int dd = 0; dd < kDpt; ++dd)
 #pragma unroll 4
-      for (int w = 0; w < kPer; ++w) {
-        const uint32_t c = cnt[(w0 + w) * kWRadix + dd];
-        cnt[(w0 + w) * kWRadix + dd] = basev;
-        basev += c;
-      }
+        for (int w = 0; w < kWarps; ++w) {
+          const uint32_t c = cnt[w * kPRadix + d0 + dd];
+          cnt[w * kPRadix + d0 + dd] = (uint16_t)basev;
+          basev += c;
+        }
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < IT; ++r) {
       const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
       if (p < m) {
-        const unsigned d = (pk[r] >> shift) & (kWRadix - 1);
-        skey[wc[d] + ((rk2[r / 2] >> (16 * (r & 1))) & 0xffffu)] = pk[r];
+        const unsigned d = (pk[r] >> shift) & (kPRadix - 1);
+        const uint32_t w = pass == 0 ? ((pk[r] >> kPDigitBits) << kPackPosBits) | p : pk[r];
+        skey[wc[d] + ((rk2[r / 2] >> (16 * (r & 1))) & 0xffffu)] = w;
       }
     }
     __syncthreads();
@@ -403,7 +416,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
 
 template <int IT, int NT = kWSortThreads>
 constexpr size_t window_sort_packed_smem() {
-  return (size_t)wsort_cfg<IT, kWSortTile, NT>::W * 4 + (size_t)kWRadix * (NT / 32) * 4;
+  return (size_t)wsort_cfg<IT, kWSortTile, NT>::W * 4 + (size_t)kPRadix * (NT / 32) * 2;
 }
 
 template <int IT, int NT = kWSortThreads>

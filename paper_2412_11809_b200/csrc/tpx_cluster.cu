@@ -832,13 +832,12 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
 
   int rc;
   const hit_src hits = r.hits;
-  // windowed sorts: 0 D = 1024 (10240-hit window, 8192 outputs), 1 packed
-  // D = 2560 (13312 / 8192: high-rate streams, whose windows span < 2^18
-  // ticks), 2 D = 2560 (10240 / 5120: wider windows), 3 D = 3072 (10240 /
-  // 4096); 4 global radix sort; 5 global union-find pipeline (internal
-  // fallback).  (A packed D = 1024 attempt does not fit the 40 Mhit/s mixed
-  // stream: ~half of its 13312-hit windows span more than 2^18 ticks.)
-  constexpr int kRadixAttempt = 4;
+  // windowed sorts: 0 packed D = 1024 (13312-hit window, 11264 outputs),
+  // 1 unpacked D = 1024 (10240 / 8192: windows spanning >= 2^27 ticks),
+  // 2 packed D = 2560 (13312 / 8192), 3 unpacked D = 2560 (10240 / 5120),
+  // 4 unpacked D = 3072 (10240 / 4096); 5 global radix sort; 6 global
+  // union-find pipeline (internal fallback)
+  constexpr int kRadixAttempt = 5;
   constexpr int kSortProbeRuns = 64;
   if (c->sort_start > 0 && ++c->runs_at_start > kSortProbeRuns) {
     c->sort_start = 0;
@@ -847,19 +846,21 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
   const int first_attempt = c->sort_start;
   nvtx_range nv_run("tpx:run");
   for (int attempt = first_attempt; attempt <= kRadixAttempt + 1; ++attempt) {
-    nvtx_range nv_sort(attempt == 0   ? "tpx:sort_window"
-                       : attempt <= 2 ? "tpx:sort_window_d2560"
-                       : attempt == 3 ? "tpx:sort_window_d3072"
+    nvtx_range nv_sort(attempt <= 1   ? "tpx:sort_window"
+                       : attempt <= 3 ? "tpx:sort_window_d2560"
+                       : attempt == 4 ? "tpx:sort_window_d3072"
                                       : "tpx:sort_fallback");
     if ((rc = reset_header(c, r))) return rc;
     if (c->profiling) cudaEventRecord(c->ev[0], r.s);
     if (attempt == 0) {
-      if ((rc = window_sort<20, kSortT0, 512>(c, r, S, hdr))) return rc;  // D = 1024
+      if ((rc = window_sort_packed<26, 11264>(c, r, S, hdr))) return rc;  // D = 1024
     } else if (attempt == 1) {
-      if ((rc = window_sort_packed<26, 8192>(c, r, S, hdr))) return rc;  // D = 2560
+      if ((rc = window_sort<20, kSortT0, 512>(c, r, S, hdr))) return rc;  // D = 1024
     } else if (attempt == 2) {
-      if ((rc = window_sort<20, kSortTm, 512>(c, r, S, hdr))) return rc;  // D = 2560
+      if ((rc = window_sort_packed<26, 8192>(c, r, S, hdr))) return rc;  // D = 2560
     } else if (attempt == 3) {
+      if ((rc = window_sort<20, kSortTm, 512>(c, r, S, hdr))) return rc;  // D = 2560
+    } else if (attempt == 4) {
       if ((rc = window_sort<20, kSortT1, 512>(c, r, S, hdr))) return rc;  // D = 3072
     } else {
       if ((rc = sort_global(c, r))) return rc;
@@ -889,7 +890,7 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
       if (attempt < kRadixAttempt && c->host_hdr->sort_bad) {  // displacement bound violated: widen / fall back
         // a packed attempt that failed on displacement (not on its 18-bit key
         // range) skips the unpacked attempt with the same bound
-        if (attempt == 1 && !(c->host_hdr->err & 8u)) ++attempt;
+        if ((attempt == 0 || attempt == 2) && !(c->host_hdr->err & 8u)) ++attempt;
         if (attempt + 1 > c->sort_start) {
           c->sort_start = attempt + 1;
           c->runs_at_start = 0;
