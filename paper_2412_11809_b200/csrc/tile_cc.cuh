@@ -186,6 +186,37 @@ __device__ __forceinline__ void s_unite(uint32_t* par, uint32_t a, uint32_t b) {
   }
 }
 
+// The same union with both finds climbing in lockstep: each step issues the
+// two parent loads together (independent), so a union costs about one find's
+// latency instead of two, and stops as soon as the two walks meet.
+__device__ __forceinline__ void s_unite_il(uint32_t* par, uint32_t a, uint32_t b) {
+  volatile uint32_t* vp = par;
+  a = vp[a];
+  b = vp[b];
+  for (;;) {
+    if (a == b) return;
+    const uint32_t pa = vp[a], pb = vp[b];
+    if (pa == a && pb == b) {  // two roots: larger under smaller
+      const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+      const uint32_t old = atomicCAS(par + hi, hi, lo);
+      if (old == hi) return;
+      a = lo;
+      b = old;  // hi was linked meanwhile: go on from its new parent
+      continue;
+    }
+    if (pa != a) {
+      const uint32_t ga = vp[pa];
+      if (ga != pa) red_min_shared(par + a, ga);
+      a = ga;
+    }
+    if (pb != b) {
+      const uint32_t gb = vp[pb];
+      if (gb != pb) red_min_shared(par + b, gb);
+      b = gb;
+    }
+  }
+}
+
 __device__ __forceinline__ uint64_t srec_key_toa(const srec* S, uint64_t i) { return __ldg(&S[i].tt) >> 16; }
 
 // First p in [lo, hi) with pred(p) (hi if none) for a monotone pred, one warp:

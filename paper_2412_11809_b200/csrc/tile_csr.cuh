@@ -377,18 +377,18 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
         }
         if (act && tgt != j) {
           if (tgt < cb) tgt = par[tgt];
-          if (atomicCAS(par + j, j, tgt) != j) s_unite(par, j, tgt);
+          if (atomicCAS(par + j, j, tgt) != j) s_unite_il(par, j, tgt);
         }
       }
       if (act) {
         if (ne <= 4) {
-          for (uint32_t q = 0; q < ne; ++q) s_unite(par, j, ((q < 2 ? exl : exh) >> (16 * (q & 1)) & 0xffffu) - kBackCap);
+          for (uint32_t q = 0; q < ne; ++q) s_unite_il(par, j, ((q < 2 ? exl : exh) >> (16 * (q & 1)) & 0xffffu) - kBackCap);
         } else {  // more than four extras (very rare): unite every tile / forward-halo neighbour
           auto all = [&](uint32_t lo, uint32_t len) {
             for (uint32_t k = 0; k < len; ++k) {
               const uint2 e = ent[lo + k];
               const uint32_t le = e.y >> 20;
-              if (csr_back_adjacent(e.y, pj) && tj - e.x <= dt32 && le >= (uint32_t)kBackCap) s_unite(par, j, le - kBackCap);
+              if (csr_back_adjacent(e.y, pj) && tj - e.x <= dt32 && le >= (uint32_t)kBackCap) s_unite_il(par, j, le - kBackCap);
             }
           };
           all(lo0, len0);
