@@ -124,6 +124,35 @@ __device__ __forceinline__ void uf_unite(uint32_t* parent, uint32_t a, uint32_t 
   }
 }
 
+// The same union with both walks climbing in lockstep (the two parent loads
+// of a step are independent, so the L2 round trips overlap) and stopping as
+// soon as they meet.  A climb step halves the path (benign race as above).
+__device__ __forceinline__ void uf_unite_il(uint32_t* parent, uint32_t a, uint32_t b) {
+  for (;;) {
+    if (a == b) return;
+    const uint32_t pa = ld_cg(parent + a), pb = ld_cg(parent + b);
+    if (pa == pb) return;
+    if (pa == a && pb == b) {  // two roots: larger under smaller
+      const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+      const uint32_t old = atomicCAS(parent + hi, hi, lo);
+      if (old == hi) return;
+      a = lo;
+      b = old;
+      continue;
+    }
+    if (pa != a) {
+      const uint32_t ga = ld_cg(parent + pa);
+      if (ga != pa) parent[a] = ga;
+      a = ga;
+    }
+    if (pb != b) {
+      const uint32_t gb = ld_cg(parent + pb);
+      if (gb != pb) parent[b] = gb;
+      b = gb;
+    }
+  }
+}
+
 // Small device -> host read-backs (run header, counts, probe samples) are
 // stored by a one-block kernel into mapped pinned memory instead of a
 // cudaMemcpyAsync: a D2H copy would queue on the copy engine behind whatever

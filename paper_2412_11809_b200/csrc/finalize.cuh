@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kListThreads) k_overflow_unions(const srec* __
       }
       if (adj) {
         if (!is_open(openbm, j)) flag_internal(hdr);
-        else uf_unite(parent_g, i, (uint32_t)j);
+        else uf_unite_il(parent_g, i, (uint32_t)j);
       }
       if (!__all_sync(kFull, in)) break;  // past the window (sorted by ToA)
     }
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kListThreads) k_pair_unions(const uint2* __res
       flag_internal(hdr);
       return;
     }
-    uf_unite(parent_g, p.x, p.y);
+    uf_unite_il(parent_g, p.x, p.y);
   }
 }
 

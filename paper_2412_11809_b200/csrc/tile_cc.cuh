@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       uint32_t xy, tj;
       auto edge = [&](uint32_t lj) {
         if (ne < kEdgeBuf) eb[ne++ * kTileThreads + threadIdx.x] = (uint16_t)lj;
-        else s_unite(par, j, lj);
+        else s_unite_il(par, j, lj);
       };
       bool back_near = false;
       {
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         const uint32_t e = b + lane;
         const uint32_t L = e < E ? owner[e] : 0u;
         const uint32_t pL = __shfl_sync(kFull, pre, L);
-        if (e < E) s_unite(par, chunk * 32 + L, eb[(e - pL) * kTileThreads + wbase + L]);
+        if (e < E) s_unite_il(par, chunk * 32 + L, eb[(e - pL) * kTileThreads + wbase + L]);
       }
     }
     __syncwarp();

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
         const bool full = ne >= kEdgeBuf;
         if (!full) eb[slot * kTh + threadIdx.x] = (uint16_t)q;
         ne += (ok & !full) ? 1u : 0u;
-        if (ok & full) s_unite(par, j, q);
+        if (ok & full) s_unite_il(par, j, q);
       };
       uint64_t hq = ~0ull;  // queue of list continuations (16 bits each, kNil-padded)
       if (act) {
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cell(tile_args
           const uint32_t e = b + lane;
           const uint32_t L = e < E ? owner[e] : 0u;
           const uint32_t pL = __shfl_sync(kFull, pre, L);
-          if (e < E) s_unite(par, chunk * 32 + L, eb[(e - pL) * kTh + wbase + L]);
+          if (e < E) s_unite_il(par, chunk * 32 + L, eb[(e - pL) * kTh + wbase + L]);
         }
       }
       __syncwarp();
