@@ -414,15 +414,30 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
   // which reuses the entry array: par is not written, so no walk races a
   // store); multi-hit marks; open marks; cross pairs (forward-halo hits rooted
   // in a tile component)
+  // the kStage walks of a thread advance in lockstep: their parent loads are
+  // independent and overlap
+  uint32_t rc[C::kStage];
 #pragma unroll
   for (int s = 0; s < C::kStage; ++s) {
     const uint32_t l = threadIdx.x + s * kTh;
-    uint32_t c = 0;
+    rc[s] = l < m ? par[l] : 0u;
+  }
+  for (;;) {
+    bool more = false;
+#pragma unroll
+    for (int s = 0; s < C::kStage; ++s) {
+      const uint32_t nx = par[rc[s]];
+      more |= nx != rc[s];
+      rc[s] = nx;
+    }
+    if (!more) break;
+  }
+#pragma unroll
+  for (int s = 0; s < C::kStage; ++s) {
+    const uint32_t l = threadIdx.x + s * kTh;
+    const uint32_t c = rc[s];
     bool joined = false;
     if (l < m) {
-      uint32_t nx;
-      c = par[l];
-      while (c != (nx = par[c])) c = nx;
       root_of[l] = (uint16_t)c;
       if (l < nt) {
         if (c != l) multi[c] = 1;
