@@ -85,8 +85,8 @@ struct csr_smem {
   static constexpr size_t accT = accN + kA * 4;                        // sum ToT
   static constexpr size_t accX = accT + kA * 4;                        // sum x
   static constexpr size_t accY = accX + kA * 4;                        // sum y
-  static constexpr size_t accTX = accY + kA * 4;                       // sum ToT*x (lo [kA], hi [kA])
-  static constexpr size_t accTY = accTX + kA * 8;                      // sum ToT*y (lo [kA], hi [kA])
+  static constexpr size_t accTX = accY + kA * 4;                       // sum ToT*x: low 16-bit halves [kA], high halves [kA]
+  static constexpr size_t accTY = accTX + kA * 8;                      // sum ToT*y: same
   static constexpr size_t accE = accTY + kA * 8;                       // min input index
   static constexpr size_t accF = accE + kA * 4;                        // first owned local idx
   static constexpr size_t accG = accF + kA * 4;                        // last owned local idx
@@ -551,8 +551,13 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
         atomicAdd(accT + slot, tot);
         atomicAdd(accX + slot, pxy & 0xffffu);
         atomicAdd(accY + slot, pxy >> 16);
-        add_u64_pair(accTX + slot, accTX + slot + C::kMulti, stx);
-        add_u64_pair(accTY + slot, accTY + slot + C::kMulti, sty);
+        // ToT*x, ToT*y (< 2^31 per run) as low and high 16-bit halves in two
+        // 32-bit sums each (<= 2048 runs per component: no overflow), so no
+        // atomic waits for its return value to propagate a carry
+        atomicAdd(accTX + slot, stx & 0xffffu);
+        atomicAdd(accTX + slot + C::kMulti, stx >> 16);
+        atomicAdd(accTY + slot, sty & 0xffffu);
+        atomicAdd(accTY + slot + C::kMulti, sty >> 16);
       }
       atomicMin(accE + slot, midx);
       if (ownm) {
@@ -590,8 +595,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
           const uint32_t cnt = accN[sl];
           const uint64_t tmin = cnt ? base + rec[accF[sl]].x : base + 0xffffffffull;
           const uint64_t tmax = cnt ? base + rec[accG[sl]].x : base;
-          const uint64_t stx = ((uint64_t)accTX[sl + C::kMulti] << 32) | accTX[sl];
-          const uint64_t sty = ((uint64_t)accTY[sl + C::kMulti] << 32) | accTY[sl];
+          const uint64_t stx = ((uint64_t)accTX[sl + C::kMulti] << 16) + accTX[sl];
+          const uint64_t sty = ((uint64_t)accTY[sl + C::kMulti] << 16) + accTY[sl];
           stage_write(dst, label, cnt, tmin, tmax, accT[sl], accX[sl], accY[sl], stx, sty);
         }
       }
