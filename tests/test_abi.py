@@ -79,6 +79,18 @@ def test_create_validates_without_gpu(lib):
     assert e.value.status == -1
 
 
+def test_tile_modes_validated_without_gpu(lib):
+    """auto / sparse / dense / cell are accepted; TPX_TILE_COLUMN (3, round 1's
+    column-bucket kernel, removed) and out-of-range modes are INVALID_ARG."""
+    import ctypes
+    c = lib.Clusterer(128)
+    for m in ("auto", "sparse", "dense", "cell"):
+        c.set_tile_mode(m)
+    for raw in (3, 5, -1):
+        assert lib._set_tile_mode(c._h, raw) == -1
+    c.close()
+
+
 def test_too_many_hits_rejected_before_any_cuda_call(lib):
     c = lib.Clusterer(128)
     with pytest.raises(lib.TpxError) as e:
