@@ -62,7 +62,8 @@ template <bool kFromHits>
 __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
     hit_src hits, const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t n,
     uint64_t toa_min, int pass, uint32_t n_tiles, const uint32_t* __restrict__ gcount, uint32_t* ticket,
-    unsigned long long* status, uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    unsigned long long* status, uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+    srec* __restrict__ s_out) {
   constexpr int kWarps = kRadixThreads / 32;
   constexpr int kPerWarp = kRadixItems * 32;
   static_assert(kRadixThreads == kRadixBins, "one look-back thread per digit");
@@ -183,8 +184,18 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
   for (uint32_t i = threadIdx.x; i < m; i += kRadixThreads) {
     const uint32_t k = skey[i];
     const uint32_t pos = gb[(k >> shift) & 0xffu] + i;
-    keys_out[pos] = k;
-    vals_out[pos] = sval[i];
+    if (s_out) {  // last pass: the sorted record itself (gathered by input index)
+      const uint32_t gi = sval[i];
+      const hit4 h = load_hit(hits + gi);
+      srec r;
+      r.tt = (h.toa << 16) | h.tot;
+      r.xy = (h.y << 16) | h.x;
+      r.idx = gi;
+      store_srec(s_out + pos, r);
+    } else {
+      keys_out[pos] = k;
+      vals_out[pos] = sval[i];
+    }
   }
 }
 

@@ -195,9 +195,12 @@ static int exclusive_scan(tpx_cluster* c, const uint32_t* in, uint64_t n, uint32
   return TPX_OK;
 }
 
+// s_out: if not null and the single-sweep path runs, its last pass writes the
+// sorted records there and *perm_out is set to a null permutation with
+// *gathered = true.
 template <typename KeyT>
 static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min, int passes, char* ws,
-                      const layout& L, uint32_t** perm_out, cudaStream_t s) {
+                      const layout& L, uint32_t** perm_out, cudaStream_t s, srec* s_out, bool* gathered) {
   KeyT* k0 = (KeyT*)(ws + L.keys0);
   KeyT* k1 = (KeyT*)(ws + L.keys1);
   uint32_t* v0 = (uint32_t*)(ws + L.vals0);
@@ -218,12 +221,13 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
       k_os_hist<<<hg, 256, 0, s>>>(hits, n, toa_min, passes, gcount);
       TPX_LAUNCHED(c);
       for (int p = 0; p < passes; ++p) {
+        srec* so = (p + 1 == passes) ? s_out : nullptr;
         if (p == 0)
           k_os_pass<true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, p, tiles, gcount, ticket,
-                                                          status, (uint32_t*)k1, v1);
+                                                          status, (uint32_t*)k1, v1, so);
         else
           k_os_pass<false><<<tiles, kRadixThreads, 0, s>>>(hits, (const uint32_t*)k0, v0, n, toa_min, p, tiles, gcount,
-                                                           ticket, status, (uint32_t*)k1, v1);
+                                                           ticket, status, (uint32_t*)k1, v1, so);
         TPX_LAUNCHED(c);
         KeyT* tk = k0;
         k0 = k1;
@@ -234,6 +238,7 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
       }
     }
     *perm_out = passes ? v0 : nullptr;
+    if (gathered) *gathered = passes > 0 && s_out;
     return TPX_OK;
   }
   for (int p = 0; p < passes; ++p) {
@@ -343,9 +348,12 @@ static int sort_global(tpx_cluster* c, const run_ptrs& r) {
   const int bits = range ? 64 - __builtin_clzll(range) : 0;
   const int passes = (bits + 7) / 8;
   uint32_t* perm = nullptr;
-  rc = (bits <= 32) ? radix_sort<uint32_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s)
-                    : radix_sort<uint64_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s);
+  bool gathered = false;
+  srec* S = (srec*)(r.ws + r.L.S);
+  rc = (bits <= 32) ? radix_sort<uint32_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s, S, &gathered)
+                    : radix_sort<uint64_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s, nullptr, nullptr);
   if (rc) return rc;
+  if (gathered) return TPX_OK;  // the last pass wrote S
   k_gather_init<<<grid_for(r.n, 256), 256, 0, r.s>>>(r.hits, perm, r.n, (srec*)(r.ws + r.L.S),
                                                      (uint32_t*)(r.ws + r.L.parent));
   TPX_LAUNCHED(c);
