@@ -13,7 +13,9 @@
 // tile's count -- keep walking -- or the inclusive prefix -- stop), then
 // publishes its own inclusive prefix and scatters digit runs to
 // consecutive global positions.  Stability of every pass keeps the final
-// order (toa, input index).
+// order (toa, input index).  The last pass writes the sorted 16-byte records
+// themselves (each gathered by its input index), so no permutation makes a
+// round trip through HBM.
 #pragma once
 #include "common.cuh"
 #include "sort.cuh"
