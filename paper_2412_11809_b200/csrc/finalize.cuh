@@ -214,31 +214,48 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
     const uint32_t cc = comp_count[t];
     const uint4* src = reinterpret_cast<const uint4*>(stage + (uint64_t)t * tile);
-    for (uint32_t q0 = 0; q0 < cc * 4; q0 += 32) {  // warp-uniform trip count
-      const uint32_t q = q0 + lane;
-      const bool valid = q < cc * 4;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (valid) v = __ldcs(src + q);
-      // the record's first word (label, size) sits in the group's first lane
-      const uint32_t label = __shfl_sync(kFull, v.x, lane & ~3u);
-      const uint32_t size = __shfl_sync(kFull, v.y, lane & ~3u);
-      if (!valid || size == 0) continue;
-      const uint32_t w = label >> 5;
-      const uint32_t bits = bitmap[w];
-      if ((q & 3) == 0) v.x = label + label_off;  // global label (sharded runs)
-      if (!((bits >> (label & 31)) & 1u)) {
-        // bit cleared by the sharded boundary merge: the record moves to the
-        // rank owning the cluster's final label (one slot per record)
-        if (!removed) continue;
-        uint32_t slot = 0;
-        if ((q & 3) == 0) slot = (uint32_t)atomicAdd(n_removed, 1ull);
-        slot = __shfl_sync(0xfu << (lane & ~3u), slot, lane & ~3u);  // the record's 4 lanes take this branch together
-        reinterpret_cast<uint4*>(removed + slot)[q & 3] = v;
-        continue;
+    // two 32-word steps per iteration: both steps' loads (record words, then
+    // bitmap words, then ordinal bases) are in flight together
+    for (uint32_t q0 = 0; q0 < cc * 4; q0 += 64) {  // warp-uniform trip count
+      uint4 v[2];
+      uint32_t label[2], size[2], bits[2], base[2];
+      bool valid[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t q = q0 + 32 * u + lane;
+        valid[u] = q < cc * 4;
+        v[u] = make_uint4(0, 0, 0, 0);
+        if (valid[u]) v[u] = __ldcs(src + q);
       }
-      const uint64_t ord = (uint64_t)wbase[w] + __popc(bits & ((1u << (label & 31)) - 1u));
-      if (ord >= capacity) continue;
-      reinterpret_cast<uint4*>(out + ord)[q & 3] = v;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        // the record's first word (label, size) sits in the group's first lane
+        label[u] = __shfl_sync(kFull, v[u].x, lane & ~3u);
+        size[u] = __shfl_sync(kFull, v[u].y, lane & ~3u);
+        valid[u] = valid[u] && size[u] != 0;
+        bits[u] = valid[u] ? bitmap[label[u] >> 5] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) base[u] = valid[u] ? wbase[label[u] >> 5] : 0u;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!valid[u]) continue;
+        const uint32_t q = q0 + 32 * u + lane;
+        if ((q & 3) == 0) v[u].x = label[u] + label_off;  // global label (sharded runs)
+        if (!((bits[u] >> (label[u] & 31)) & 1u)) {
+          // bit cleared by the sharded boundary merge: the record moves to the
+          // rank owning the cluster's final label (one slot per record)
+          if (!removed) continue;
+          uint32_t slot = 0;
+          if ((q & 3) == 0) slot = (uint32_t)atomicAdd(n_removed, 1ull);
+          slot = __shfl_sync(0xfu << (lane & ~3u), slot, lane & ~3u);  // the record's 4 lanes take this branch together
+          reinterpret_cast<uint4*>(removed + slot)[q & 3] = v[u];
+          continue;
+        }
+        const uint64_t ord = (uint64_t)base[u] + __popc(bits[u] & ((1u << (label[u] & 31)) - 1u));
+        if (ord >= capacity) continue;
+        reinterpret_cast<uint4*>(out + ord)[q & 3] = v[u];
+      }
     }
   }
 }
