@@ -214,21 +214,22 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += nw) {
     const uint32_t cc = comp_count[t];
     const uint4* src = reinterpret_cast<const uint4*>(stage + (uint64_t)t * tile);
-    // two 32-word steps per iteration: both steps' loads (record words, then
-    // bitmap words, then ordinal bases) are in flight together
-    for (uint32_t q0 = 0; q0 < cc * 4; q0 += 64) {  // warp-uniform trip count
-      uint4 v[2];
-      uint32_t label[2], size[2], bits[2], base[2];
-      bool valid[2];
+    // kU 32-word steps per iteration: their loads (record words, then bitmap
+    // words, then ordinal bases) are in flight together
+    constexpr int kU = 4;
+    for (uint32_t q0 = 0; q0 < cc * 4; q0 += 32 * kU) {  // warp-uniform trip count
+      uint4 v[kU];
+      uint32_t label[kU], size[kU], bits[kU], base[kU];
+      bool valid[kU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const uint32_t q = q0 + 32 * u + lane;
         valid[u] = q < cc * 4;
         v[u] = make_uint4(0, 0, 0, 0);
         if (valid[u]) v[u] = __ldcs(src + q);
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kU; ++u) {
         // the record's first word (label, size) sits in the group's first lane
         label[u] = __shfl_sync(kFull, v[u].x, lane & ~3u);
         size[u] = __shfl_sync(kFull, v[u].y, lane & ~3u);
@@ -236,9 +237,9 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
         bits[u] = valid[u] ? bitmap[label[u] >> 5] : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) base[u] = valid[u] ? wbase[label[u] >> 5] : 0u;
+      for (int u = 0; u < kU; ++u) base[u] = valid[u] ? wbase[label[u] >> 5] : 0u;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kU; ++u) {
         if (!valid[u]) continue;
         const uint32_t q = q0 + 32 * u + lane;
         if ((q & 3) == 0) v[u].x = label[u] + label_off;  // global label (sharded runs)
