@@ -140,17 +140,20 @@ __global__ void __launch_bounds__(256) k_variant_large(variant_args a) {
         for (uint32_t base = p; base > o0;) {
           const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
           bool in = false, isadj = false;
+          uint32_t r1 = 0;
           if (q != 0xffffffffu && q >= o0) {
             const hit4 hq = load_hit(a.ih + q);
             in = hq.toa + a.window >= ti;
             isadj = in && var_adjacent(hi, hq);
             if (isadj) {
-              const uint32_t r = var_find(a.par, q);
-              if (var_pred(a, r, ti)) a.stamp[r] = p + 1;
+              r1 = var_find(a.par, q);
+              if (var_pred(a, r1, ti)) a.stamp[r1] = p + 1;
             }
           }
+          // the list keeps the candidate's ROOT: nothing links before pass 3,
+          // so passes 2 and 3 need no second walk
           const unsigned bm = __ballot_sync(kFull, isadj);
-          if (isadj && nadj + __popc(bm) <= kVarAdjCap) adj[nadj + __popc(bm & lanemask_lt())] = q;
+          if (isadj && nadj + __popc(bm) <= kVarAdjCap) adj[nadj + __popc(bm & lanemask_lt())] = r1;
           nadj += __popc(bm);
           if (!__any_sync(kFull, in)) break;
           base = base > 32 ? base - 32 : 0;
@@ -170,7 +173,14 @@ __global__ void __launch_bounds__(256) k_variant_large(variant_args a) {
           }
         };
         if (listed) {
-          for (uint32_t i = lane; i < nadj; i += 32) take(adj[i]);
+          for (uint32_t i = lane; i < nadj; i += 32) {
+            const uint32_t r = adj[i];  // a root (pass 1)
+            if (a.stamp[r] == p + 1) {
+              tmin = min(tmin, r);
+              mn = min(mn, a.cmin[r]);
+              mx = max(mx, a.cmax[r]);
+            }
+          }
         } else {
           for (uint32_t base = p; base > o0;) {
             const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
@@ -199,7 +209,10 @@ __global__ void __launch_bounds__(256) k_variant_large(variant_args a) {
             if (a.stamp[r] == p + 1 && r != tmin) a.par[r] = tmin;  // same value from every lane
           };
           if (listed) {
-            for (uint32_t i = lane; i < nadj; i += 32) link(adj[i]);
+            for (uint32_t i = lane; i < nadj; i += 32) {
+              const uint32_t r = adj[i];
+              if (a.stamp[r] == p + 1 && r != tmin) a.par[r] = tmin;  // same value from every lane
+            }
           } else {
             for (uint32_t base = p; base > o0;) {
               const uint32_t q = base > lane ? base - 1 - lane : 0xffffffffu;
