@@ -621,8 +621,29 @@ def run_ours_multi(args):
     t = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=rdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
+    # ---- roofline of the dominant kernel on every rank (one extra profiled
+    # run after the timed ones: stage events on the run stream), the slowest
+    # rank's launch reported
+    sc.ctx.set_profiling(1)
+    rp = step(d_hits)
+    torch.cuda.synchronize()
+    sc.ctx.set_profiling(0)
+    stg = rp.stats.get("stage_ms", {}) or {}
+    t_tile = float(stg.get("tile_cc", 0.0))
+    b_alg_hit = 16 + 4 + 64 / max(nr / max(rp.n_clusters, 1), 1e-9)
+    tt = torch.tensor([t_tile], device=rdev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_tile_max = float(tt.item())
+    roof = None
+    if t_tile_max > 0:
+        peak, peak_src = _peaks()
+        achieved = b_alg_hit * nr / (t_tile_max * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "tile_cc", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "alg_bytes_per_hit": round(b_alg_hit, 3), "launch_ms": round(t_tile_max, 4),
+                "note": "per GPU: one rank's block over its slowest rank's tile-kernel launch"}
     gathered = [None] * ws
-    dist.all_gather_object(gathered, {"rank": rank, "n": nr, "ms": ms_local,
+    dist.all_gather_object(gathered, {"rank": rank, "n": nr, "ms": ms_local, "tile_ms": t_tile,
                                       **{k_: v for k_, v in st.items() if k_ != "tile_phase_cycles"}})
     if rank == 0:
         out = {
@@ -638,6 +659,7 @@ def run_ours_multi(args):
                     "h2d_bytes_per_step": nr * 16, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
                     "note": "per-rank bytes (rank 0); time = max over ranks"},
             "gpu_launches": launches_step * args.steps,
+            "roofline": roof,
             "per_rank": gathered,
             "clocks": clocks,
             "gen_seconds": round(gen_s, 2),
