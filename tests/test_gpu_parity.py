@@ -241,6 +241,28 @@ def test_radix_fallback_edges(tpx, n, toa_max):
     assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
 
 
+def test_packed_sort_wide_windows_fall_back(tpx):
+    """A stream whose 13312-hit windows span more than 2^28 ticks (but less
+    than 2^31): the packed window sort declines (err bit 3) and the unpacked
+    kernel with the same displacement bound sorts it -- still bit-exact."""
+    rng = np.random.default_rng(77)
+    n = 60_000
+    h = np.zeros(n, dtype=tpxgen.HIT_DTYPE)
+    toa = np.sort(rng.integers(0, (1 << 31) - (1 << 26), n))  # 13312-hit windows span ~4.7e8 ticks
+    # light readout disorder: swap a few neighbours
+    idx = rng.integers(0, n - 1, n // 20)
+    toa[idx], toa[idx + 1] = toa[idx + 1].copy(), toa[idx].copy()
+    h["toa"] = toa
+    h["x"] = rng.integers(0, 64, n)
+    h["y"] = rng.integers(0, 64, n)
+    h["tot"] = rng.integers(1, 1024, n)
+    c, gl, gf, k = _fresh(tpx, h, 1 << 22, 64, 64)
+    st = c.stats()
+    assert st["sort_path"] == 0 and st["sort_retries"] >= 1
+    rl, rf = oracle.cluster(h, 1 << 22, 64, 64)
+    assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
+
+
 def test_sort_attempt_memory(tpx):
     """A failed displacement bound is detected right after the sort (no
     clustering pass on a wrong order) and the context starts at the attempt
