@@ -17,6 +17,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libtpxcluster.so")
+# bounds-checked build (device asserts, -DTPX_CHECKED): tests only
+CHECKED_LIB = os.path.join(LIBDIR, "checked", "libtpxcluster.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
@@ -35,31 +37,34 @@ def _sources():
                   + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile the library if any source is newer than the .so."""
-    if not force and not needs_build():
-        return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Compile the library if any source is newer than the .so.  checked=True
+    builds the bounds-checked variant (TPX_BOUND device asserts) into
+    lib/checked/ instead; the product never loads it."""
+    lib = CHECKED_LIB if checked else LIB
+    if not force and not needs_build(lib):
+        return lib
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     tus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-shared", "-o", tmp, *tus]
+    tmp = lib + f".tmp{os.getpid()}"
+    extra = ["-DTPX_CHECKED"] if checked else []
+    cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-shared", "-o", tmp, *tus]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libtpxcluster.so")
+        raise RuntimeError(f"nvcc failed building {lib}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -5,6 +5,18 @@
 
 #include "tpx_cluster.h"
 
+// Bounds checks of the checked build (build.py --checked: -DTPX_CHECKED, a
+// separate lib/checked/libtpxcluster.so used only by tests/test_gpu_checked.py):
+// a failing check is a device-side assert (file, line, failing index printed;
+// the launch reports cudaErrorAssert).  The product build compiles them out.
+#ifdef TPX_CHECKED
+#undef NDEBUG
+#include <cassert>
+#define TPX_BOUND(i, n) assert((unsigned long long)(i) < (unsigned long long)(n))
+#else
+#define TPX_BOUND(i, n) ((void)0)
+#endif
+
 namespace tpx {
 
 constexpr unsigned kFull = 0xffffffffu;

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(const tpx_cluster_feature
         }
         const uint64_t ord = (uint64_t)base[u] + __popc(bits[u] & ((1u << (label[u] & 31)) - 1u));
         if (ord >= capacity) continue;
+        TPX_BOUND(label[u], (uint64_t)n_tiles * tile);  // labels are input indices
         reinterpret_cast<uint4*>(out + ord)[q & 3] = v[u];
       }
     }

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
     const uint32_t p = warp * kPerWarp + r * 32 + lane;
     if (p < m) {
       const uint32_t q = w[(key[r] >> shift) & 0xffu] + rk[r];
+      TPX_BOUND(q, m);
       skey[q] = key[r];
       sval[q] = val[r];
     }
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
   for (uint32_t i = threadIdx.x; i < m; i += kRadixThreads) {
     const uint32_t k = skey[i];
     const uint32_t pos = gb[(k >> shift) & 0xffu] + i;
+    TPX_BOUND(pos, n);
     if (s_out) {  // last pass: the sorted record itself (gathered by input index)
       const uint32_t gi = sval[i];
       const hit4 h = load_hit(hits + gi);

@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
       if (p < m) {
         const unsigned d = (pk[r] >> shift) & (kPRadix - 1);
         const uint32_t w = pass == 0 ? ((pk[r] >> kPDigitBits) << kPackPosBits) | p : pk[r];
+        TPX_BOUND(wc[d] + ((rk2[r / 2] >> (16 * (r & 1))) & 0xffffu), m);
         skey[wc[d] + ((rk2[r / 2] >> (16 * (r & 1))) & 0xffffu)] = w;
       }
     }
@@ -405,6 +406,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
   const uint32_t cnt_out = (uint32_t)min((uint64_t)T, n - k0);
   for (uint32_t j = threadIdx.x; j < cnt_out; j += NT) {
     const uint64_t gi = ws + (skey[ofs + j] & ((1u << kPackPosBits) - 1));
+    TPX_BOUND(ofs + j, m);
+    TPX_BOUND(gi, we);
+    TPX_BOUND(k0 + j, n);
     hit4 h = load_hit(hits + gi);
     srec r;
     r.tt = (h.toa << 16) | h.tot;

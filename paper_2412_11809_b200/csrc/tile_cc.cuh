@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       return make_uint2((uint32_t)(srec_toa(r) - base), r.xy);
     };
     auto insert = [&](uint32_t l, uint2 e) {
+      TPX_BOUND(l, C::kFwdMax);
       stoa[l] = e.x;
       if (l < nt) sxy[l] = e.y;
       par[l] = l;
@@ -537,6 +538,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
     // a tile hit finds the earlier hits next to it through its 9 lookups
     // instead of scanning the back halo
     auto insert_back = [&](uint32_t l, uint2 e) {
+      TPX_BOUND(l, SL::kIdx);
       stoa[l] = e.x;
       const uint32_t pix = (e.y >> 16) * W + (e.y & 0xffffu);
       uint32_t h = slot_of_pixel(pix);
@@ -634,6 +636,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
             if ((cur >> kHeadBits) != pix) continue;
             uint32_t best = 0xffffu;
             for (uint32_t q = cur & kHeadMask; q != kNil; q = nxt[q]) {
+              TPX_BOUND(q, SL::kIdx);
               if (q >= m) back_near |= tj - stoa[q] <= dt32;  // back-halo hit (earlier)
               else if (q > j && q < best) best = q;
             }
@@ -670,6 +673,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
         const uint32_t e = b + lane;
         const uint32_t L = e < E ? owner[e] : 0u;
         const uint32_t pL = __shfl_sync(kFull, pre, L);
+        TPX_BOUND(e < E ? e - pL : 0u, kEdgeBuf);
         if (e < E) s_unite_il(par, chunk * 32 + L, eb[(e - pL) * kTileThreads + wbase + L]);
       }
     }
@@ -681,6 +685,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   // ---- flatten (read-only root walk; every stored value is a final root)
   for (uint32_t l = threadIdx.x; l < m; l += kTileThreads) {
     const uint32_t p0 = par[l];
+    TPX_BOUND(p0, m);
     uint32_t c = p0, nx;
     while (c != (nx = par[c])) c = nx;
     if (c != p0) red_min_shared(par + l, c);  // atomic: other threads' walks read par[l]
@@ -758,7 +763,11 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
     const uint32_t j = threadIdx.x + q * kTileThreads;
     if (j < nt) {
       const uint32_t r = par[j];
-      if (((csize2[r >> 1] >> ((r & 1) * 16)) & 0xffffu) >= 2) mem[coff[r] + atomicAdd(&ccur[r], 1u)] = (uint16_t)j;
+      if (((csize2[r >> 1] >> ((r & 1) * 16)) & 0xffffu) >= 2) {
+        const uint32_t mi = coff[r] + atomicAdd(&ccur[r], 1u);
+        TPX_BOUND(mi, kTile);
+        mem[mi] = (uint16_t)j;
+      }
     }
   }
   __syncthreads();
@@ -781,6 +790,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
           for (uint32_t k = 0; k < sz; ++k) f.add(stile[mem[o + k]], a.n_owned);
         }
         mlabel[j] = f.midx;
+        TPX_BOUND(t0 + crank[j], t1);
         stage_write(a.stage + t0 + crank[j], f.midx, f.cnt, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
                     f.sty);
       }
@@ -798,6 +808,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
     f.warp_reduce();
     if (lane == 0) {
       mlabel[r] = f.midx;
+      TPX_BOUND(t0 + crank[r], t1);
       stage_write(a.stage + t0 + crank[r], f.midx, f.cnt, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
                   f.sty);
     }

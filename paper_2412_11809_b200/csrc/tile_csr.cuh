@@ -222,9 +222,11 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     key[s] = 0;
     if (l < m) {
       const uint32_t xy = rr[s].xy;
+      TPX_BOUND(l, C::kFwdMax);
       rec[l] = make_uint2((uint32_t)(srec_toa(rr[s]) - base), xy);
       par[l] = l;
       const uint32_t c = cell_of(xy);
+      TPX_BOUND(c >> 1, C::kCntWords);
       const uint32_t sh = (c & 1u) * 16u;
       const uint32_t old = atomicAdd(cnt32 + (c >> 1), 1u << sh);
       key[s] = (c << 12) | ((old >> sh) & 0xfffu);
@@ -283,9 +285,11 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     if (l < m) {
       const uint2 e = rec[l];
       const uint32_t k = key[s];
+      TPX_BOUND(off16[k >> 12] + (k & 0xfffu), kBackCap + C::kFwdMax);
       ent[off16[k >> 12] + (k & 0xfffu)] = make_uint2(e.x, csr_pack(e.y, l + kBackCap));
     }
   }
+  TPX_BOUND(back_in ? off16[keyb >> 12] + (keyb & 0xfffu) : 0u, kBackCap + C::kFwdMax);
   if (back_in) ent[off16[keyb >> 12] + (keyb & 0xfffu)] = make_uint2(tb, csr_pack(xyb, kBackCap - (uint32_t)(t0 - bpos)));
   __syncthreads();
   TPX_PHASE(3);
@@ -335,6 +339,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
       uint32_t bm = kNone, ne = 0;
       uint32_t exl = 0, exh = 0;  // up to four extra neighbours (16-bit staged indices), newest in the low half of exl
       auto visit = [&](uint32_t p, bool valid) {
+        TPX_BOUND(p, (SL::total - SL::ent) / 8);
         const uint2 e = ent[p];  // p may run past the ranges (masked by valid; inside the CTA's smem)
         const bool edge = valid & csr_back_adjacent(e.y, pj) & (tj - e.x <= dt32);
         const uint32_t le = e.y >> 20;
@@ -376,6 +381,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
           if (tgt >= cb) tgt = t2;
         }
         if (act && tgt != j) {
+          TPX_BOUND(tgt, m);
+          TPX_BOUND(j, m);
           if (tgt < cb) tgt = par[tgt];
           if (atomicCAS(par + j, j, tgt) != j) s_unite_il(par, j, tgt);
         }
@@ -399,6 +406,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
           }
         }
         if (j < nt) {
+          TPX_BOUND(j, kT);
           uint8_t fl = (ftrunc && tj >= fwd_thr) ? 3 : 0;  // window continues past the halo
           // an earlier neighbour in the back halo, or one that was not staged
           if (bm < (uint32_t)kBackCap || (btrunc && tj <= dt32)) fl |= 1;
@@ -438,6 +446,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     const uint32_t c = rc[s];
     bool joined = false;
     if (l < m) {
+      TPX_BOUND(c, m);
+      TPX_BOUND(c <= l ? 0u : 1u, 1u);  // roots are the smallest staged index of their tree
       root_of[l] = (uint16_t)c;
       if (l < nt) {
         if (c != l) multi[c] = 1;
@@ -478,6 +488,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
         crank[j] = (uint16_t)(ex & 0xffffu);
         const bool mu = packed[q] >> 16;
         const uint32_t sl = ex >> 16;
+        TPX_BOUND(j, kT);
+        TPX_BOUND(mu ? sl : 0u, C::kMulti);
         aslot[j] = mu ? (uint16_t)sl : (uint16_t)0xffffu;
         if (mu) {
           accN[sl] = 0;
@@ -544,6 +556,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
       }
     }
     if (lane == e && slot != 0xffffu) {
+      TPX_BOUND(slot, C::kMulti);
       const uint32_t cnt = __popc(ownm);
       const uint32_t jbase = j - lane;
       if (cnt) {
@@ -583,6 +596,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
       const uint32_t sl = aslot[r];
       label = sl == 0xffffu ? tidx[q] : accE[sl];
       if (is_root) {
+        TPX_BOUND(t0 + crank[j], t1);
         tpx_cluster_features* dst = a.stage + t0 + crank[j];
         if (sl == 0xffffu) {
           const bool own = tidx[q] < a.n_owned;
@@ -593,6 +607,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
                       tot * x, tot * y);
         } else {
           const uint32_t cnt = accN[sl];
+          TPX_BOUND(cnt ? accF[sl] : 0u, nt);
+          TPX_BOUND(cnt ? accG[sl] : 0u, nt);
           const uint64_t tmin = cnt ? base + rec[accF[sl]].x : base + 0xffffffffull;
           const uint64_t tmax = cnt ? base + rec[accG[sl]].x : base;
           const uint64_t stx = ((uint64_t)accTX[sl + C::kMulti] << 16) + accTX[sl];
@@ -603,6 +619,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
     }
     const uint64_t pos = t0 + j;
     if (is_root) {
+      TPX_BOUND(pos, a.n);
       if (!open && label < a.n_owned) {
         set_label_bit(a.bitmap, label);
         if (a.first_of_label) a.first_of_label[label] = (uint32_t)pos;  // grouping: cluster's first sorted position

@@ -80,6 +80,11 @@ def test_sanitizer_clean(abi_run, tmp_path, case, tool):
     cmd += [abi_run, str(hits), str(dt), str(W), str(H), str(lab), str(ft), str(mode), str(variant)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     log = r.stdout[-4000:] + r.stderr[-4000:]
+    if r.returncode == 86 and "closed" in log:
+        # the GPU pool replaced compute-sanitizer by a stub that refuses to run
+        # (exit 86); tests/test_gpu_checked.py covers the same cases with the
+        # library's own bounds-checked build
+        pytest.skip("compute-sanitizer is closed on this GPU pool: " + log.strip().splitlines()[-1][:160])
     assert r.returncode == 0, log
     if tool != "racecheck":  # racecheck prints its own summary line instead
         assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, log
