@@ -70,6 +70,42 @@ __device__ __forceinline__ hit4 load_hit(const tpx_hit* h) {
   return r;
 }
 
+// L2 eviction-priority hints (createpolicy + ld/st .L2::cache_hint): the
+// window sort loads its window "evict last" so the record gather at the end
+// of the CTA finds the lines still in L2, and gathers / stores the records it
+// will not touch again "evict first".
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_v4_hint(const void* ptr, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_v4_hint(void* ptr, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ hit4 load_hit_hint(const tpx_hit* h, uint64_t pol) {
+  const uint4 v = ldg_v4_hint(h, pol);
+  hit4 r;
+  r.toa = (uint64_t)v.x | ((uint64_t)v.y << 32);
+  r.x = v.z & 0xffffu;
+  r.y = v.z >> 16;
+  r.tot = v.w & 0xffffu;
+  return r;
+}
+
 // Input of the sort kernels: one array, or two concatenated segments (the
 // sharded path sorts [owned hits | halo received from the next rank] without
 // copying the caller's owned hits): element i is a[i] for i < na, else

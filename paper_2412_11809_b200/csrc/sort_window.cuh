@@ -250,6 +250,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort(hit_src hits, uin
 // wide with 16-bit counters (ranks and offsets are < 2^16 in a 13312-hit
 // window), so a 20-bit window range -- the 40 Mhit/s mixed stream's 13312-hit
 // windows span up to ~3.2e5 ticks -- still sorts in two passes.
+#ifndef TPX_SORT_L2HINT
+#define TPX_SORT_L2HINT 1
+#endif
 constexpr int kPackPosBits = 14;
 constexpr int kPDigitBits = 10;
 constexpr int kPRadix = 1 << kPDigitBits;
@@ -280,12 +283,19 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
   uint32_t pk[IT];
   uint32_t mn = 0xffffffffu, mx = 0;
   unsigned bad = 0, far = 0;
+#if TPX_SORT_L2HINT
+  const uint64_t pol_keep = l2_policy_evict_last();
+#endif
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const uint32_t p = warp * C::PER_WARP + r * 32 + lane;
     pk[r] = 0;
     if (p < m) {
+#if TPX_SORT_L2HINT
+      hit4 h = load_hit_hint(hits + (ws + p), pol_keep);
+#else
       hit4 h = load_hit(hits + (ws + p));
+#endif
       const uint64_t d = h.toa - org;
       far |= (d >> 32) != 0;
       pk[r] = (uint32_t)d;
@@ -404,17 +414,28 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
   // ---- write the middle T records (window-local ranks [k0-ws, k0-ws+T))
   const uint32_t ofs = (uint32_t)(k0 - ws);
   const uint32_t cnt_out = (uint32_t)min((uint64_t)T, n - k0);
+#if TPX_SORT_L2HINT
+  const uint64_t pol_drop = l2_policy_evict_first();
+#endif
   for (uint32_t j = threadIdx.x; j < cnt_out; j += NT) {
     const uint64_t gi = ws + (skey[ofs + j] & ((1u << kPackPosBits) - 1));
     TPX_BOUND(ofs + j, m);
     TPX_BOUND(gi, we);
     TPX_BOUND(k0 + j, n);
+#if TPX_SORT_L2HINT
+    hit4 h = load_hit_hint(hits + gi, pol_drop);
+#else
     hit4 h = load_hit(hits + gi);
+#endif
     srec r;
     r.tt = (h.toa << 16) | h.tot;
     r.xy = (h.y << 16) | h.x;
     r.idx = (uint32_t)gi;
+#if TPX_SORT_L2HINT
+    stg_v4_hint(out + k0 + j, make_uint4((uint32_t)r.tt, (uint32_t)(r.tt >> 32), r.xy, r.idx), pol_drop);
+#else
     store_srec(out + k0 + j, r);
+#endif
   }
 }
 
