@@ -17,6 +17,18 @@
 #define TPX_BOUND(i, n) ((void)0)
 #endif
 
+// Sorted records gathered per thread and step (their loads in flight
+// together) at the end of the window sort and of the last radix pass.
+// Measured (A/B of builds, one box): window sort 1 / 2 / 4 -> mixed 200M
+// 4.037 / 4.07 / 4.041 ms (Timepix4 6.716 / 6.649 / 6.679); radix 1 / 2 / 4
+// -> heavy-ion 50M sort 2.411 / 2.327 / 2.303 ms.
+#ifndef TPX_WSORT_GATHER_U
+#define TPX_WSORT_GATHER_U 1
+#endif
+#ifndef TPX_RADIX_GATHER_U
+#define TPX_RADIX_GATHER_U 4
+#endif
+
 namespace tpx {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -86,7 +98,7 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
 }
 __device__ __forceinline__ uint4 ldg_v4_hint(const void* ptr, uint64_t pol) {
   uint4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+  asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(ptr), "l"(pol));
   return v;

@@ -184,19 +184,36 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
     }
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < m; i += kRadixThreads) {
-    const uint32_t k = skey[i];
-    const uint32_t pos = gb[(k >> shift) & 0xffu] + i;
-    TPX_BOUND(pos, n);
-    if (s_out) {  // last pass: the sorted record itself (gathered by input index)
-      const uint32_t gi = sval[i];
-      const hit4 h = load_hit(hits + gi);
-      srec r;
-      r.tt = (h.toa << 16) | h.tot;
-      r.xy = (h.y << 16) | h.x;
-      r.idx = gi;
-      store_srec(s_out + pos, r);
-    } else {
+  if (s_out) {  // last pass: the sorted records themselves (gathered by input index, kGU per thread in flight)
+    constexpr int kGU = TPX_RADIX_GATHER_U;
+    for (uint32_t i0 = threadIdx.x; i0 < m; i0 += kGU * kRadixThreads) {
+      uint4 v[kGU];
+      uint32_t pos[kGU], gi[kGU];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        const uint32_t i = i0 + u * kRadixThreads;
+        if (i < m) {
+          pos[u] = gb[(skey[i] >> shift) & 0xffu] + i;
+          gi[u] = sval[i];
+          TPX_BOUND(pos[u], n);
+          v[u] = __ldg(reinterpret_cast<const uint4*>(hits + gi[u]));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        const uint32_t i = i0 + u * kRadixThreads;
+        if (i < m) {
+          const uint64_t toa = (uint64_t)v[u].x | ((uint64_t)v[u].y << 32);
+          const uint64_t tt = (toa << 16) | (v[u].w & 0xffffu);
+          *reinterpret_cast<uint4*>(s_out + pos[u]) = make_uint4((uint32_t)tt, (uint32_t)(tt >> 32), v[u].z, gi[u]);
+        }
+      }
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < m; i += kRadixThreads) {
+      const uint32_t k = skey[i];
+      const uint32_t pos = gb[(k >> shift) & 0xffu] + i;
+      TPX_BOUND(pos, n);
       keys_out[pos] = k;
       vals_out[pos] = sval[i];
     }

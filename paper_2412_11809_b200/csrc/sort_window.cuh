@@ -417,25 +417,49 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_window_sort_packed(hit_src hi
 #if TPX_SORT_L2HINT
   const uint64_t pol_drop = l2_policy_evict_first();
 #endif
-  for (uint32_t j = threadIdx.x; j < cnt_out; j += NT) {
-    const uint64_t gi = ws + (skey[ofs + j] & ((1u << kPackPosBits) - 1));
-    TPX_BOUND(ofs + j, m);
-    TPX_BOUND(gi, we);
-    TPX_BOUND(k0 + j, n);
+  // kGU records per thread in flight: their shared-memory positions, then
+  // their gathers, then their stores
+  constexpr int kGU = TPX_WSORT_GATHER_U;
+  for (uint32_t j0 = threadIdx.x; j0 < cnt_out; j0 += kGU * NT) {
+    uint4 v[kGU];
+    uint32_t gi[kGU];
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const uint32_t j = j0 + u * NT;
+      gi[u] = 0;
+      if (j < cnt_out) {
+        TPX_BOUND(ofs + j, m);
+        gi[u] = skey[ofs + j] & ((1u << kPackPosBits) - 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const uint32_t j = j0 + u * NT;
+      if (j < cnt_out) {
+        TPX_BOUND(ws + gi[u], we);
 #if TPX_SORT_L2HINT
-    hit4 h = load_hit_hint(hits + gi, pol_drop);
+        v[u] = ldg_v4_hint(hits + (ws + gi[u]), pol_drop);
 #else
-    hit4 h = load_hit(hits + gi);
+        v[u] = __ldg(reinterpret_cast<const uint4*>(hits + (ws + gi[u])));
 #endif
-    srec r;
-    r.tt = (h.toa << 16) | h.tot;
-    r.xy = (h.y << 16) | h.x;
-    r.idx = (uint32_t)gi;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const uint32_t j = j0 + u * NT;
+      if (j < cnt_out) {
+        TPX_BOUND(k0 + j, n);
+        // tpx_hit {toa, x | y << 16, tot | reserved << 16} -> srec {toa << 16 | tot, y << 16 | x, index}
+        const uint64_t toa = (uint64_t)v[u].x | ((uint64_t)v[u].y << 32);
+        const uint64_t tt = (toa << 16) | (v[u].w & 0xffffu);
+        const uint4 o = make_uint4((uint32_t)tt, (uint32_t)(tt >> 32), v[u].z, (uint32_t)(ws + gi[u]));
 #if TPX_SORT_L2HINT
-    stg_v4_hint(out + k0 + j, make_uint4((uint32_t)r.tt, (uint32_t)(r.tt >> 32), r.xy, r.idx), pol_drop);
+        stg_v4_hint(out + k0 + j, o, pol_drop);
 #else
-    store_srec(out + k0 + j, r);
+        *reinterpret_cast<uint4*>(out + k0 + j) = o;
 #endif
+      }
+    }
   }
 }
 
