@@ -282,7 +282,9 @@ struct tile_smem_hash {
   static constexpr size_t mem = stile + (size_t)kTile * 16;             // u16   [kTile]
   static constexpr size_t big = mem + (size_t)kTile * 2;                // u16   [kTile]
   static constexpr size_t mlabel = big + (size_t)kTile * 2;             // u32   [kTile]
-  static_assert(mlabel + (size_t)kTile * 4 <= region_a, "reduction arrays alias region A");
+  static constexpr size_t bacc = mlabel + (size_t)kTile * 4;           // big_acc [kMaxBig] (segmented big components)
+  static constexpr size_t kMaxBig = kTile / 24 + 1;                     // kBigComp = 24
+  static_assert(bacc + kMaxBig * 64 <= region_a, "reduction arrays alias region A");
   static constexpr size_t hb = region_a;                                // uint2 [kBackCap]
   static constexpr size_t par = hb + (size_t)kBackCap * 8;              // u32   [kFwdMax]
   static constexpr size_t csize = par + (size_t)kFwdMax * 4;            // u32   [kTile/2] (u16 pairs)
@@ -303,7 +305,17 @@ template <class C>
 constexpr size_t tile_smem_bytes() {
   return tile_smem_layout<C>::total;
 }
-constexpr uint32_t kBigComp = 24;  // components this large are reduced by a whole warp
+constexpr uint32_t kBigComp = 24;  // components this large are reduced by whole warps
+constexpr uint32_t kBigSeg = 128;  // member hits per warp work item of a large component
+
+// Partial-sum accumulator of one large component (reduced in kBigSeg-hit
+// segments by several warps, merged by shared-memory atomics; the warp that
+// merges the last segment writes the record).  64 bytes.
+struct big_acc {
+  unsigned long long tot, sx, sy, stx, sty;
+  uint32_t tmin, tmax, midx, cnt, segbase, done;
+};
+static_assert(sizeof(big_acc) == 64, "big_acc is 64 bytes");
 
 // Block-wide exclusive scan (kTileThreads threads) of one u32 per thread.
 template <int kTileThreads>
@@ -411,7 +423,8 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   uint8_t* hflag = sm + SL::hflag;  // per tile hit: bit0 open mark, bit1 overflow
   __shared__ uint64_t s_meta[8];
   __shared__ uint32_t s_wsum[kTileThreads / 32];
-  __shared__ uint32_t s_chunk, s_nbig, s_bigq;
+  __shared__ uint32_t s_chunk, s_nbig, s_bigq, s_nseg;
+  big_acc* bacc = reinterpret_cast<big_acc*>(sm + SL::bacc);
 
   const uint64_t n = a.n, dt = a.dt;
   const srec* __restrict__ S = a.S;
@@ -770,6 +783,37 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       }
     }
   }
+  if (warp == 0) {  // large components: segment counts -> work-item prefix; accumulators
+    const uint32_t nbig = s_nbig;
+    uint32_t run = 0;
+    for (uint32_t g0 = 0; g0 < nbig; g0 += 32) {
+      const uint32_t bi = g0 + lane;
+      uint32_t ns = 0;
+      if (bi < nbig) {
+        TPX_BOUND(bi, SL::kMaxBig);
+        const uint32_t r = big[bi], sz = (csize2[r >> 1] >> ((r & 1) * 16)) & 0xffffu;
+        ns = (sz + kBigSeg - 1) / kBigSeg;
+      }
+      uint32_t x = ns;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= (unsigned)o) x += y;
+      }
+      if (bi < nbig) {
+        big_acc& A = bacc[bi];
+        A.tot = A.sx = A.sy = A.stx = A.sty = 0;
+        A.tmin = 0xffffffffu;
+        A.tmax = 0;
+        A.midx = 0xffffffffu;
+        A.cnt = 0;
+        A.segbase = run + x - ns;
+        A.done = 0;
+      }
+      run += __shfl_sync(kFull, x, 31);
+    }
+    if (lane == 0) s_nseg = run;
+  }
   __syncthreads();
   TPX_PHASE(6);
 
@@ -796,21 +840,64 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       }
     }
   }
+  // large components: kBigSeg-hit segments as warp work items (a 5000-hit
+  // blob is spread over ~40 warps instead of holding one warp while the
+  // others wait at the barrier)
+  const uint32_t nbig = s_nbig, nseg = s_nseg;
   for (;;) {
-    uint32_t bi = 0;
-    if (lane == 0) bi = atomicAdd(&s_bigq, 1u);
-    bi = __shfl_sync(kFull, bi, 0);
-    if (bi >= s_nbig) break;
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(&s_bigq, 1u);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= nseg) break;
+    uint32_t bi = 0;  // the component whose segments contain t: (# segbase <= t) - 1
+    for (uint32_t g0 = 0; g0 < nbig; g0 += 32) {
+      const bool le = g0 + lane < nbig && bacc[g0 + lane].segbase <= t;
+      bi += __popc(__ballot_sync(kFull, le));
+    }
+    bi -= 1;
+    TPX_BOUND(bi, nbig);
     const uint32_t r = big[bi], sz = (csize2[r >> 1] >> ((r & 1) * 16)) & 0xffffu, o = coff[r];
+    const uint32_t seg = t - bacc[bi].segbase, ns = (sz + kBigSeg - 1) / kBigSeg;
+    const uint32_t k1 = min(sz, (seg + 1) * kBigSeg);
     feat_acc f;
     f.init();
-    for (uint32_t k = lane; k < sz; k += 32) f.add(stile[mem[o + k]], a.n_owned);
+    for (uint32_t k = seg * kBigSeg + lane; k < k1; k += 32) f.add(stile[mem[o + k]], a.n_owned);
     f.warp_reduce();
     if (lane == 0) {
-      mlabel[r] = f.midx;
-      TPX_BOUND(t0 + crank[r], t1);
-      stage_write(a.stage + t0 + crank[r], f.midx, f.cnt, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
-                  f.sty);
+      bool last = ns == 1;
+      if (!last) {
+        big_acc& A = bacc[bi];
+        atomicAdd(&A.tot, (unsigned long long)f.tot);
+        atomicAdd(&A.sx, (unsigned long long)f.sx);
+        atomicAdd(&A.sy, (unsigned long long)f.sy);
+        atomicAdd(&A.stx, (unsigned long long)f.stx);
+        atomicAdd(&A.sty, (unsigned long long)f.sty);
+        atomicMin(&A.tmin, f.tmin);
+        atomicMax(&A.tmax, f.tmax);
+        atomicMin(&A.midx, f.midx);
+        atomicAdd(&A.cnt, f.cnt);
+        __threadfence_block();
+        last = atomicAdd(&A.done, 1u) == ns - 1;
+        if (last) {  // every other segment merged before its done increment
+          __threadfence_block();
+          const volatile big_acc& V = A;
+          f.tot = V.tot;
+          f.sx = V.sx;
+          f.sy = V.sy;
+          f.stx = V.stx;
+          f.sty = V.sty;
+          f.tmin = V.tmin;
+          f.tmax = V.tmax;
+          f.midx = V.midx;
+          f.cnt = V.cnt;
+        }
+      }
+      if (last) {
+        mlabel[r] = f.midx;
+        TPX_BOUND(t0 + crank[r], t1);
+        stage_write(a.stage + t0 + crank[r], f.midx, f.cnt, base + f.tmin, base + f.tmax, f.tot, f.sx, f.sy, f.stx,
+                    f.sty);
+      }
     }
   }
   __syncthreads();
