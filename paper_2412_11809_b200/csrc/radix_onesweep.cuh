@@ -73,7 +73,6 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
   __shared__ uint32_t sval[kRadixTile];
   __shared__ uint32_t wc[kWarps * kRadixBins];  // warp-major digit counters, then tile-local offsets
   __shared__ uint32_t gb[kRadixBins];           // global position - tile-local position, by digit
-  __shared__ uint32_t dsum[kWarps];
   __shared__ uint32_t s_tile;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const int shift = 8 * pass;

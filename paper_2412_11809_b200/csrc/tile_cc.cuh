@@ -446,7 +446,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       s_meta[0] = b0;
       s_meta[2] = srec_key_toa(S, b0);               // base: the smallest staged ToA
       s_meta[3] = btrunc ? 1u : 0u;
-      s_meta[5] = t0 ? srec_key_toa(S, t0 - 1) : 0;  // ToA of the previous tile's last hit
       s_chunk = 0;
       s_nbig = 0;
       s_bigq = 0;
@@ -611,7 +610,6 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   // local index > j.  Dense: per neighbouring pixel one hash probe sequence,
   // then the smallest local index > j in its list.  Either way the work per
   // hit is independent of the window density.
-  const uint64_t prev_last = s_meta[5];
   const uint64_t first_unstaged = s_meta[4];
   const uint32_t wmax = W - 1;
   const uint32_t n_chunks = (nt + 31) / 32;

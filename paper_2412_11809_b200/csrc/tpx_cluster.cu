@@ -240,7 +240,8 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
     *perm_out = passes ? v0 : nullptr;
     if (gathered) *gathered = passes > 0 && s_out;
     return TPX_OK;
-  }
+  } else {
+  // 64-bit keys (ToA spans >= 2^32 ticks): histogram + scan + scatter per pass
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
     if (p == 0) {
@@ -251,15 +252,7 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
     TPX_LAUNCHED(c);
     int rc = exclusive_scan(c, hist, (uint64_t)tiles * kRadixBins, hist, partials, nullptr, s);
     if (rc) return rc;
-    if constexpr (sizeof(KeyT) == 4) {
-      if (p == 0) {
-        k_radix_scatter_tile<true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, shift, hist,
-                                                                   tiles, k1, v1);
-      } else {
-        k_radix_scatter_tile<false><<<tiles, kRadixThreads, 0, s>>>(hits, k0, v0, n, toa_min, shift, hist, tiles,
-                                                                    k1, v1);
-      }
-    } else if (p == 0) {
+    if (p == 0) {
       k_radix_scatter<KeyT, true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, shift, hist,
                                                                   tiles, k1, v1);
     } else {
@@ -276,6 +269,7 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
   }
   *perm_out = passes ? v0 : nullptr;
   return TPX_OK;
+  }
 }
 
 struct run_ptrs {
@@ -839,7 +833,6 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
   dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
 
   int rc;
-  const hit_src hits = r.hits;
   // windowed sorts: 0 packed D = 1024 (13312-hit window, 11264 outputs),
   // 1 unpacked D = 1024 (10240 / 8192: windows spanning >= 2^27 ticks),
   // 2 packed D = 2560 (13312 / 8192), 3 unpacked D = 2560 (10240 / 5120),
