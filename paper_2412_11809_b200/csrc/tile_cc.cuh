@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   __shared__ uint64_t s_meta[8];
   __shared__ uint32_t s_wsum[kTileThreads / 32];
   __shared__ uint32_t s_chunk, s_nbig, s_bigq, s_nseg;
+  __shared__ uint32_t s_app[3];  // output phase: open components / open hits / overflow of this CTA, then their list bases
   big_acc* bacc = reinterpret_cast<big_acc*>(sm + SL::bacc);
 
   const uint64_t n = a.n, dt = a.dt;
@@ -434,9 +435,17 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   long long t_phase = clock64();
 
-  // ---- halo ranges (32-ary warp searches in the sorted stream: warp 0 the
-  // back halo, warp 1 the forward halo), sort verification
-  if (warp == 0) {
+  // ---- halo ranges: precomputed by k_tile_bounds (one load), else 32-ary
+  // warp searches in the sorted stream (warp 0 the back halo, warp 1 the
+  // forward halo) while the other warps clear the index
+  if (a.tile_meta) {
+    if (threadIdx.x < 8) s_meta[threadIdx.x] = a.tile_meta[(uint64_t)blockIdx.x * 8 + threadIdx.x];
+    if (threadIdx.x == 0) {
+      s_chunk = 0;
+      s_nbig = 0;
+      s_bigq = 0;
+    }
+  } else if (warp == 0) {
     const uint64_t toa_first = srec_key_toa(S, t0);
     const uint64_t blim = t0 > (uint64_t)kBackCap ? t0 - kBackCap : 0;
     // back halo: first position with toa + dt >= toa_first
@@ -471,6 +480,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
     hflag[j] = 0;
   }
   for (uint32_t w = threadIdx.x; w < kTile / 2; w += kTileThreads) csize2[w] = 0;
+  if (threadIdx.x < 3) s_app[threadIdx.x] = 0;
   __syncthreads();
   TPX_PHASE(0);
   const uint64_t b0 = s_meta[0], f1 = s_meta[1], base = s_meta[2];
@@ -901,7 +911,44 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
   __syncthreads();
   TPX_PHASE(7);
 
-  // ---- outputs: labels, bitmap, open lists
+  // ---- outputs: labels, bitmap, open lists.  The open-list appends are
+  // aggregated per CTA (warp counts -> shared offsets -> one global atomic
+  // per list and CTA): with half of a heavy-ion stream's hits open, per-warp
+  // global appends queue on the three list counters.
+  uint32_t wofs[kItemsPerThread][3];
+#pragma unroll
+  for (int q = 0; q < kItemsPerThread; ++q) {
+    const uint32_t j = threadIdx.x + q * kTileThreads;
+    const bool v = j < nt;
+    bool is_root = false, open = false;
+    if (v) {
+      const uint32_t r = par[j];
+      is_root = r == j;
+      open = copen[r] != 0;
+    }
+    const bool ovf = v && (hflag[j] & 2u);
+    const unsigned mc = __ballot_sync(kFull, is_root && open), mh = __ballot_sync(kFull, v && open),
+                   mo = __ballot_sync(kFull, ovf);
+    uint32_t b0 = 0, b1 = 0, b2 = 0;
+    if (lane == 0) {
+      if (mc) b0 = atomicAdd(&s_app[0], (uint32_t)__popc(mc));
+      if (mh) b1 = atomicAdd(&s_app[1], (uint32_t)__popc(mh));
+      if (mo) b2 = atomicAdd(&s_app[2], (uint32_t)__popc(mo));
+    }
+    const unsigned lt = lanemask_lt();
+    wofs[q][0] = __shfl_sync(kFull, b0, 0) + __popc(mc & lt);
+    wofs[q][1] = __shfl_sync(kFull, b1, 0) + __popc(mh & lt);
+    wofs[q][2] = __shfl_sync(kFull, b2, 0) + __popc(mo & lt);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t c0 = s_app[0], c1 = s_app[1], c2 = s_app[2];
+    s_app[0] = c0 ? (uint32_t)atomicAdd(&a.hdr->n_open_comps, (unsigned long long)c0) : 0u;
+    s_app[1] = c1 ? (uint32_t)atomicAdd(&a.hdr->n_open_hits, (unsigned long long)c1) : 0u;
+    s_app[2] = c2 ? (uint32_t)atomicAdd(&a.hdr->n_overflow, (unsigned long long)c2) : 0u;
+  }
+  __syncthreads();
+  const uint32_t base_oc = s_app[0], base_oh = s_app[1], base_ov = s_app[2];
 #pragma unroll
   for (int q = 0; q < kItemsPerThread; ++q) {
     const uint32_t j = threadIdx.x + q * kTileThreads;
@@ -926,19 +973,16 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_cc(tile_args a
       const unsigned om = __ballot_sync(kFull, v && open);
       if (lane_id() == 0 && om) a.openbm[pos >> 5] = om;
     }
-    const uint32_t oc = warp_append(is_root && open, &a.hdr->n_open_comps);
-    if (is_root && open) a.open_comps[oc] = (uint32_t)pos;
-    const uint32_t oh = warp_append(v && open, &a.hdr->n_open_hits);
+    if (is_root && open) a.open_comps[base_oc + wofs[q][0]] = (uint32_t)pos;
     const bool ovf = v && (hflag[j] & 2u);
-    const uint32_t ov = warp_append(ovf, &a.hdr->n_overflow);
     if (v) {
       if (open) {
         a.parent_g[pos] = (uint32_t)(t0 + r);
-        a.open_hits[oh] = (uint32_t)pos;
+        a.open_hits[base_oh + wofs[q][1]] = (uint32_t)pos;
       } else {
         store_label(a.labels, a.n_owned, a.lm, rq[q].idx, label);
       }
-      if (ovf) a.overflow[ov] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
+      if (ovf) a.overflow[base_ov + wofs[q][2]] = make_uint2((uint32_t)pos, (uint32_t)(t0 + m));  // staged part done in-tile
     }
   }
   TPX_PHASE(8);

@@ -443,9 +443,14 @@ static int cluster_sorted(tpx_cluster* c, const run_ptrs& r) {
   a.tile_meta = nullptr;
   a.first_of_label = c->want_first ? (uint32_t*)(ws + L.minidx) : nullptr;
   a.lm = r.lm;
-  if (r.dense)
-    k_tile_cc<tile_dense><<<n_tiles_of(r.n, tile_dense::kTile), tile_dense::kThreads, tile_smem_bytes<tile_dense>(),
-                            r.s>>>(a);
+  if (r.dense) {
+    const uint32_t nt = n_tiles_of(r.n, tile_dense::kTile);
+    a.tile_meta = (const uint64_t*)(ws + L.tmeta);
+    k_tile_bounds<tile_dense><<<(nt + 7) / 8, 256, 0, r.s>>>(S, r.n, c->dt, nt, r.sort_T, (uint64_t*)(ws + L.tmeta),
+                                                            hdr);
+    TPX_LAUNCHED(c);
+    k_tile_cc<tile_dense><<<nt, tile_dense::kThreads, tile_smem_bytes<tile_dense>(), r.s>>>(a);
+  }
   else if (r.csr) {
     static_assert(csr_sparse::kTile == cell_sparse::kTile && csr_sparse::kHalo == cell_sparse::kHalo, "shared bounds");
     const uint32_t nt = n_tiles_of(r.n, csr_sparse::kTile);
