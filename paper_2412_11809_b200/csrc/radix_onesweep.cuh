@@ -40,17 +40,29 @@ struct os_layout {
 };
 
 // Digit totals of every pass (one read of the hits).
-__global__ void __launch_bounds__(256) k_os_hist(hit_src hits, uint64_t n, uint64_t toa_min, int passes,
-                                                 uint32_t* __restrict__ gcount) {
+__global__ void __launch_bounds__(256) k_os_hist(hit_src hits, uint64_t n, const unsigned long long* base_ptr,
+                                                 int passes, uint32_t* __restrict__ gcount, uint32_t width,
+                                                 uint32_t height, dev_hdr* hdr) {
   __shared__ uint32_t h[kOsPasses][kRadixBins];
   for (int i = threadIdx.x; i < kOsPasses * kRadixBins; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
+  const uint64_t toa_min = *base_ptr;
+  // validate (fused): coordinates / ToA range, and every key inside
+  // [base, base + 2^32) when the base was guessed (hdr != nullptr)
+  unsigned bad = 0, out = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = (uint32_t)(load_hit(hits + i).toa - toa_min);
+    const hit4 hi = load_hit(hits + i);
+    const uint64_t d = hi.toa - toa_min;
+    if (hdr) {
+      bad |= (hi.x >= width) | (hi.y >= height) | (hi.toa >> 48 != 0);
+      out |= (hi.toa < toa_min) | ((d >> 32) != 0);
+    }
+    const uint32_t k = (uint32_t)d;
 #pragma unroll
     for (int p = 0; p < kOsPasses; ++p)
       if (p < passes) atomicAdd(&h[p][(k >> (8 * p)) & 0xffu], 1u);
   }
+  if (hdr && __any_sync(kFull, bad | out) && lane_id() == 0) atomicOr(&hdr->err, (bad ? 1u : 0u) | (out ? 16u : 0u));
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadixBins; i += blockDim.x) {
     const uint32_t v = (&h[0][0])[i];
@@ -63,7 +75,7 @@ __global__ void __launch_bounds__(256) k_os_hist(hit_src hits, uint64_t n, uint6
 template <bool kFromHits>
 __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
     hit_src hits, const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t n,
-    uint64_t toa_min, int pass, uint32_t n_tiles, const uint32_t* __restrict__ gcount, uint32_t* ticket,
+    const unsigned long long* base_ptr, int pass, uint32_t n_tiles, const uint32_t* __restrict__ gcount, uint32_t* ticket,
     unsigned long long* status, uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
     srec* __restrict__ s_out) {
   constexpr int kWarps = kRadixThreads / 32;
@@ -91,7 +103,7 @@ __global__ void __launch_bounds__(kRadixThreads, TPX_OS_MINB) k_os_pass(
     if (p < m) {
       const uint64_t i = tbase + p;
       if constexpr (kFromHits) {
-        key[r] = (uint32_t)(load_hit(hits + i).toa - toa_min);
+        key[r] = (uint32_t)(load_hit(hits + i).toa - *base_ptr);
         val[r] = (uint32_t)i;
       } else {
         key[r] = keys_in[i];

@@ -14,13 +14,15 @@ struct dev_hdr {
   unsigned int err;          // bit 0: coordinate / ToA range violation; bit 1: internal;
                              // bit 2: a sort window spans >= 2^32 ticks (windowed sort impossible)
                              // bit 3: a packed sort window's ToA range exceeds 28 bits
+                             // bit 4: a ToA outside [radix_base, radix_base + 2^32) (speculative radix base)
   unsigned int sort_bad;     // windowed-sort verification failures
   unsigned long long n_clusters;
   unsigned long long n_pairs;       // cross-tile union pairs
   unsigned long long n_open_comps;  // components touching a tile border
   unsigned long long n_open_hits;   // hits of those components
   unsigned long long n_overflow;    // hits whose window left the staged halo
-  unsigned long long pad[8];
+  unsigned long long radix_base;    // key origin of the radix fallback (toa - radix_base < 2^32)
+  unsigned long long pad[7];
   unsigned long long phase_cycles[16];  // k_tile_cc per-phase clock totals (profiling)
 };
 static_assert(sizeof(dev_hdr) == 256, "dev_hdr layout");
@@ -50,6 +52,29 @@ __global__ void __launch_bounds__(kMMThreads) k_validate_minmax(hit_src hits, ui
     atomicMin(&hdr->toa_min, mn);
     atomicMax(&hdr->toa_max, mx);
     if (bad) atomicOr(&hdr->err, 1u);
+  }
+}
+
+// Guessed key origin of the radix fallback: the smallest ToA of the first
+// kRadixBaseSample hits less 2^28 ticks (t-ordered input: no hit precedes its
+// neighbourhood by anything near that).  The histogram kernel checks every key
+// against it (err bit 4) and validates the hits, so the ToA range needs no
+// separate pass and no read-back before the sort; a stream that breaks the
+// guess is re-sorted with the exact minimum.
+constexpr uint32_t kRadixBaseSample = 8192;
+constexpr unsigned long long kRadixBaseMargin = 1ull << 28;
+__global__ void __launch_bounds__(256) k_radix_base(hit_src hits, uint64_t n, dev_hdr* hdr) {
+  __shared__ unsigned long long red[8];
+  unsigned long long mn = ~0ull;
+  const uint64_t m = n < kRadixBaseSample ? n : kRadixBaseSample;
+  for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) mn = min(mn, (unsigned long long)load_hit(hits + i).toa);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+  if (lane_id() == 0) red[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mn = min(mn, red[w]);
+    hdr->radix_base = mn == ~0ull ? 0ull : (mn > kRadixBaseMargin ? mn - kRadixBaseMargin : 0ull);
   }
 }
 

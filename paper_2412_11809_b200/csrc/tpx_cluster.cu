@@ -200,7 +200,8 @@ static int exclusive_scan(tpx_cluster* c, const uint32_t* in, uint64_t n, uint32
 // *gathered = true.
 template <typename KeyT>
 static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min, int passes, char* ws,
-                      const layout& L, uint32_t** perm_out, cudaStream_t s, srec* s_out, bool* gathered) {
+                      const layout& L, uint32_t** perm_out, cudaStream_t s, srec* s_out, bool* gathered,
+                      const unsigned long long* base_ptr = nullptr, dev_hdr* vhdr = nullptr) {
   KeyT* k0 = (KeyT*)(ws + L.keys0);
   KeyT* k1 = (KeyT*)(ws + L.keys1);
   uint32_t* v0 = (uint32_t*)(ws + L.vals0);
@@ -218,15 +219,17 @@ static int radix_sort(tpx_cluster* c, hit_src hits, uint64_t n, uint64_t toa_min
       unsigned long long* status = (unsigned long long*)(sc + os_layout::status);
       TPX_CUDA(cudaMemsetAsync(sc, 0, os_layout::bytes(tiles), s));
       const uint32_t hg = tiles < 148 * 8 ? tiles : 148 * 8;
-      k_os_hist<<<hg, 256, 0, s>>>(hits, n, toa_min, passes, gcount);
+      // key origin on the device (base_ptr): the exact minimum, or a guess
+      // the histogram checks (vhdr: validation fused into the histogram)
+      k_os_hist<<<hg, 256, 0, s>>>(hits, n, base_ptr, passes, gcount, c->width, c->height, vhdr);
       TPX_LAUNCHED(c);
       for (int p = 0; p < passes; ++p) {
         srec* so = (p + 1 == passes) ? s_out : nullptr;
         if (p == 0)
-          k_os_pass<true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, toa_min, p, tiles, gcount, ticket,
+          k_os_pass<true><<<tiles, kRadixThreads, 0, s>>>(hits, nullptr, nullptr, n, base_ptr, p, tiles, gcount, ticket,
                                                           status, (uint32_t*)k1, v1, so);
         else
-          k_os_pass<false><<<tiles, kRadixThreads, 0, s>>>(hits, (const uint32_t*)k0, v0, n, toa_min, p, tiles, gcount,
+          k_os_pass<false><<<tiles, kRadixThreads, 0, s>>>(hits, (const uint32_t*)k0, v0, n, base_ptr, p, tiles, gcount,
                                                            ticket, status, (uint32_t*)k1, v1, so);
         TPX_LAUNCHED(c);
         KeyT* tk = k0;
@@ -328,10 +331,24 @@ static int readback_sync(tpx_cluster* c, void* dst, const void* dev, size_t byte
 }
 
 // Global LSD radix sort into S (fallback when the windowed sort cannot prove
-// its displacement bound).  Needs the ToA range first: one extra host sync.
-static int sort_global(tpx_cluster* c, const run_ptrs& r) {
+// its displacement bound).  First with a guessed key origin (k_radix_base;
+// 4 passes, validation and the range check fused into the histogram, no host
+// sync); if the guess fails (err bit 4, seen at the run's post-sort
+// read-back), exact: the ToA range first (one extra host sync), then
+// ceil(bits / 8) passes from the true minimum.
+static int sort_global(tpx_cluster* c, const run_ptrs& r, bool exact) {
   nvtx_range nv("tpx:sort_radix");
   dev_hdr* hdr = (dev_hdr*)(r.ws + r.L.hdr);
+  srec* S = (srec*)(r.ws + r.L.S);
+  if (!exact) {
+    k_radix_base<<<1, 256, 0, r.s>>>(r.hits, r.n, hdr);
+    TPX_LAUNCHED(c);
+    uint32_t* perm = nullptr;
+    bool gathered = false;
+    int rc = radix_sort<uint32_t>(c, r.hits, r.n, 0, 4, r.ws, r.L, &perm, r.s, S, &gathered, &hdr->radix_base, hdr);
+    (void)gathered;  // 4 passes with s_out: the last pass wrote S
+    return rc;
+  }
   const int g = grid_for(r.n, kMMThreads) < 148 * 8 ? grid_for(r.n, kMMThreads) : 148 * 8;
   k_validate_minmax<<<g, kMMThreads, 0, r.s>>>(r.hits, r.n, c->width, c->height, hdr);
   TPX_LAUNCHED(c);
@@ -343,8 +360,8 @@ static int sort_global(tpx_cluster* c, const run_ptrs& r) {
   const int passes = (bits + 7) / 8;
   uint32_t* perm = nullptr;
   bool gathered = false;
-  srec* S = (srec*)(r.ws + r.L.S);
-  rc = (bits <= 32) ? radix_sort<uint32_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s, S, &gathered)
+  rc = (bits <= 32) ? radix_sort<uint32_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s, S, &gathered,
+                                           &hdr->toa_min)
                     : radix_sort<uint64_t>(c, r.hits, r.n, toa_min, passes, r.ws, r.L, &perm, r.s, nullptr, nullptr);
   if (rc) return rc;
   if (gathered) return TPX_OK;  // the last pass wrote S
@@ -850,6 +867,7 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
     c->runs_at_start = 0;
   }
   const int first_attempt = c->sort_start;
+  bool radix_exact = false;  // the guessed radix key origin failed: exact range first
   nvtx_range nv_run("tpx:run");
   for (int attempt = first_attempt; attempt <= kRadixAttempt + 1; ++attempt) {
     nvtx_range nv_sort(attempt <= 1   ? "tpx:sort_window"
@@ -869,7 +887,7 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
     } else if (attempt == 4) {
       if ((rc = window_sort<20, kSortT1, 512>(c, r, S, hdr))) return rc;  // D = 3072
     } else {
-      if ((rc = sort_global(c, r))) return rc;
+      if ((rc = sort_global(c, r, radix_exact))) return rc;
     }
     c->stats.sort_path = attempt >= kRadixAttempt ? 1 : 0;
     // one small read-back after the sort: validation and window-sort status
@@ -889,6 +907,11 @@ static int run_core(tpx_cluster* c, run_ptrs& r) {
       if ((rc = read_header(c, r))) return rc;  // synchronises the stream: the probe samples are in as well
       if (probe_on) memcpy(hprobe, c->host_scratch, sizeof(hprobe));
       if (c->host_hdr->err & 1u) return TPX_ERR_COORD_RANGE;
+      if (attempt >= kRadixAttempt && !radix_exact && (c->host_hdr->err & 16u)) {  // ToA outside the guessed key range
+        radix_exact = true;
+        --attempt;
+        continue;
+      }
       if (attempt < kRadixAttempt && (c->host_hdr->err & 4u)) {  // >= 2^32-tick window: radix, this run only
         attempt = kRadixAttempt - 1;
         continue;

@@ -241,6 +241,27 @@ def test_radix_fallback_edges(tpx, n, toa_max):
     assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
 
 
+@pytest.mark.parametrize("shape", ["early_outlier", "wide_range"])
+def test_radix_guessed_base_falls_back(tpx, shape):
+    """The radix fallback first guesses its key origin (smallest ToA of the
+    first 8192 hits less 2^28 ticks, sort.cuh k_radix_base) and checks every
+    key against it; a stream that breaks the guess -- a hit far earlier than
+    the first ones, or a ToA range beyond 2^32 ticks from the guess -- is
+    re-sorted from the exact minimum, bit-exact either way."""
+    rng = np.random.default_rng(7 if shape == "early_outlier" else 8)
+    n = 30_000
+    h = tpxgen.random_small(rng, n, 16, 16, 1 << 20)
+    h["toa"] += np.uint64(1 << 34)
+    if shape == "early_outlier":
+        h["toa"][n - 5] = 3  # ~2^34 ticks before everything else, at the end of the stream
+    else:
+        h["toa"][n // 2:] += np.uint64(1 << 33)  # range > 2^32 ticks: 64-bit keys
+    c, gl, gf, k = _fresh(tpx, h, 64, 16, 16)
+    assert c.stats()["sort_path"] == 1
+    rl, rf = oracle.cluster(h, 64, 16, 16)
+    assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
+
+
 def test_packed_sort_wide_windows_fall_back(tpx):
     """A stream whose 13312-hit windows span more than 2^28 ticks (but less
     than 2^31): the packed window sort declines (err bit 3) and the unpacked
