@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(256) k_os_hist(hit_src hits, uint64_t n, const
     for (int p = 0; p < kOsPasses; ++p)
       if (p < passes) atomicAdd(&h[p][(k >> (8 * p)) & 0xffu], 1u);
   }
-  if (hdr && __any_sync(kFull, bad | out) && lane_id() == 0) atomicOr(&hdr->err, (bad ? 1u : 0u) | (out ? 16u : 0u));
+  if (hdr) {  // the warp's flags, not lane 0's own
+    const unsigned wb = __ballot_sync(kFull, bad), wo = __ballot_sync(kFull, out);
+    if ((wb | wo) && lane_id() == 0) atomicOr(&hdr->err, (wb ? 1u : 0u) | (wo ? 16u : 0u));
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadixBins; i += blockDim.x) {
     const uint32_t v = (&h[0][0])[i];

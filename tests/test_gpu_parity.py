@@ -226,6 +226,50 @@ def test_disorder_stress(tpx):
     assert np.array_equal(gl, rl) and gf.tobytes() == rf.tobytes()
 
 
+def test_context_reuse_across_changing_streams(tpx):
+    """One context through streams that break what its previous runs learnt:
+    the remembered sort attempt (sort_start) and tile configuration meet more
+    disorder, heavy-ion windows, a beam pause wider than 2^32 ticks (the
+    radix fallback's guessed key origin fails), a calm stream again, and an
+    invalid coordinate after the radix path became the start (validation
+    fused into the radix histogram must still flag it); every run bit-exact,
+    the error reported, the context usable afterwards."""
+    c = tpx.Clusterer(320)
+    streams = [
+        ("mixed", tpxgen.generate("mixed", n_hits=1_000_000, seed=61)),
+        ("mixed again", tpxgen.generate("mixed", n_hits=1_000_000, seed=62)),
+        ("heavy-ion windows", tpxgen.generate("heavyion", n_hits=600_000, seed=63)),
+        ("sparse again", tpxgen.generate("mixed", n_hits=700_000, seed=64)),
+        ("600 us disorder: window sort fails", tpxgen.generate("mixed", n_hits=800_000, seed=65,
+                                                               disorder_ticks=384_000)),
+        ("clean again", tpxgen.generate("mixed", n_hits=900_000, seed=66)),
+    ]
+    pause = tpxgen.generate("mixed", n_hits=600_000, seed=67)
+    pause["toa"][300_000:] += np.uint64(1 << 33)  # beam pause: a window spans > 2^32 ticks
+    streams.append(("beam pause", pause))
+    streams.append(("clean after the pause", tpxgen.generate("mixed", n_hits=500_000, seed=68)))
+    for name, h in streams:
+        d = torch.from_numpy(np.ascontiguousarray(h).view(np.uint8).reshape(-1)).cuda()
+        labels, feats, k = c.run(d, n=len(h))
+        torch.cuda.synchronize()
+        rl, rf = oracle.cluster(h, 320)
+        assert k == len(rf), name
+        assert np.array_equal(labels.cpu().numpy().view(np.uint32)[:len(h)], rl), name
+        assert tpx.features_to_numpy(feats).tobytes() == rf.tobytes(), name
+    bad = tpxgen.generate("mixed", n_hits=200_000, seed=69)
+    bad["x"][150_000] = 300  # outside the 256-pixel sensor
+    d = torch.from_numpy(np.ascontiguousarray(bad).view(np.uint8).reshape(-1)).cuda()
+    with pytest.raises(tpx.TpxError) as e:
+        c.run(d, n=len(bad))
+    assert e.value.status == -3  # TPX_ERR_COORD_RANGE
+    h = tpxgen.generate("mixed", n_hits=400_000, seed=70)  # and the context still works
+    d = torch.from_numpy(np.ascontiguousarray(h).view(np.uint8).reshape(-1)).cuda()
+    labels, feats, k = c.run(d, n=len(h))
+    rl, rf = oracle.cluster(h, 320)
+    assert np.array_equal(labels.cpu().numpy().view(np.uint32)[:len(h)], rl)
+    assert tpx.features_to_numpy(feats).tobytes() == rf.tobytes()
+
+
 @pytest.mark.parametrize("n,toa_max", [(12_289, 1 << 14), (40_961, (1 << 23) + 5), (100_003, (1 << 31) - 3),
                                          ((1 << 20) + 7, 1 << 20), (300_001, (1 << 24) + 1)])
 def test_radix_fallback_edges(tpx, n, toa_max):
@@ -253,7 +297,9 @@ def test_radix_guessed_base_falls_back(tpx, shape):
     h = tpxgen.random_small(rng, n, 16, 16, 1 << 20)
     h["toa"] += np.uint64(1 << 34)
     if shape == "early_outlier":
-        h["toa"][n - 5] = 3  # ~2^34 ticks before everything else, at the end of the stream
+        # 2^30 ticks before everything else, at the end of the stream: taken
+        # modulo 2^32 from the guessed origin its key would sort it last
+        h["toa"][n - 5] = (1 << 34) - (1 << 30)
     else:
         h["toa"][n // 2:] += np.uint64(1 << 33)  # range > 2^32 ticks: 64-bit keys
     c, gl, gf, k = _fresh(tpx, h, 64, 16, 16)
