@@ -70,7 +70,10 @@ struct csr_cfg {
   static_assert(kCntWords % (4 * kThreads) == 0, "scan: uint4 words per thread");
   static_assert(kTile % ::tpx::kTile == 0 && kTile <= kMaxTile, "stage slots");
 };
-using csr_sparse = csr_cfg<2048, 512, TPX_CELL_HALO, 2>;                 // 2x2-pixel cells, 128 x 128
+using csr_sparse = csr_cfg<2048, 512, TPX_CELL_HALO, 2>;
+#ifndef TPX_CSR_JUMPS
+#define TPX_CSR_JUMPS 2  // pointer-jumping rounds of the in-chunk hook targets (swept 0/1/2/3/5: 2 fastest)
+#endif                 // 2x2-pixel cells, 128 x 128
 constexpr uint32_t kCsrMaxCoord = 1023;  // 10-bit coordinate fields in the entry word
 
 // Shared-memory carve-up, bytes.  Region A holds the cell counters / offsets
@@ -370,13 +373,16 @@ __global__ void __launch_bounds__(C::kThreads, C::kBlocks) k_tile_csr(tile_args 
         for (uint32_t k = 0; k < Vw; ++k) visit(w0 + k + (k >= wl0 ? jump : 0u), k < V);
       }
       // hook target: the smallest earlier neighbour; chains inside the chunk
-      // are shortened by pointer jumping over the lanes (5 rounds cover 32),
-      // a target in an earlier chunk by one hop to its current parent
+      // are shortened by pointer jumping over the lanes (TPX_CSR_JUMPS rounds:
+      // two shorten a chain 4-fold, which measured faster than the 5 rounds
+      // that collapse any 32-lane chain -- the unions after the hook climb
+      // what is left), a target in an earlier chunk by one hop to its current
+      // parent
       {
         const uint32_t cb = chunk * 32;
         uint32_t tgt = (bm != kNone && bm >= (uint32_t)kBackCap) ? bm - kBackCap : j;
 #pragma unroll
-        for (int r = 0; r < 5; ++r) {
+        for (int r = 0; r < TPX_CSR_JUMPS; ++r) {
           const uint32_t t2 = __shfl_sync(kFull, tgt, (tgt - cb) & 31u);
           if (tgt >= cb) tgt = t2;
         }
