@@ -306,7 +306,7 @@ constexpr size_t tile_smem_bytes() {
   return tile_smem_layout<C>::total;
 }
 constexpr uint32_t kBigComp = 24;  // components this large are reduced by whole warps
-constexpr uint32_t kBigSeg = 128;  // member hits per warp work item of a large component
+constexpr uint32_t kBigSeg = 256;  // member hits per warp work item of a large component (swept 64 / 128 / 256 / 512 / 1024: 256)
 
 // Partial-sum accumulator of one large component (reduced in kBigSeg-hit
 // segments by several warps, merged by shared-memory atomics; the warp that
